@@ -1,0 +1,176 @@
+/*
+ * gb.h -- C-ABI of libgb: batched retrieval in the Gripon-Berrou clustered
+ * associative memory (GBNN), arXiv:1303.7032, on NVIDIA B200 (sm_100a).
+ *
+ * The paper's problem statement has two operations, storing and retrieving
+ * (PAPER.md L35-37).  This header exposes exactly those, plus the handle
+ * lifecycle and the plumbing a multi-GPU caller needs (W exposure for an
+ * NCCL broadcast / MAX all-reduce).
+ *
+ * Conventions:
+ *  - 0-based clusters, neurons and symbols (reading R1).  A message or probe
+ *    is uint16_t[C]; symbol in [0, L), GB_ERASED (0xFFFF) marks an erased
+ *    cluster of a probe ("(m_1, m_2, ?, ?)").
+ *  - Cluster padding: each cluster occupies Wc = ceil(L/32) 32-bit words,
+ *    Lp = 32*Wc neuron slots; n_padded = C*Lp.  Neuron (c, l) has padded
+ *    index i = c*Lp + l (the paper's i = (c-1)L + l of L310 with padding).
+ *    Padding neurons never activate and have no edges.
+ *  - A decoded state is uint32_t[C*Wc]: bit (l % 32) of word c*Wc + l/32 is
+ *    v_(c,l); padding bits are 0.
+ *  - Every pointer argument is a plain pointer.  For gb_store and gb_decode
+ *    buffers may be device pointers (on the handle's device) or host
+ *    pointers (pageable or pinned); host buffers are staged through the
+ *    library's device scratch and the call then blocks until the results are
+ *    back in host memory.  Device-pointer calls are asynchronous and
+ *    stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
+ *  - The caller owns all input/output buffers.  The library owns W (u8 and
+ *    bit-packed) and its scratch.
+ *  - Errors: functions return GB_OK (0) or a negative GB_E* code and set a
+ *    thread-local message readable with gb_last_error().  No exception or
+ *    abort crosses the ABI.  There is no CPU fallback: without a usable
+ *    sm_100 device every compute call fails with GB_ECUDA/GB_EUNSUPPORTED.
+ */
+#ifndef GB_H
+#define GB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gb_net gb_net;
+
+enum {
+    GB_OK = 0,
+    GB_EINVAL = -1,        /* bad argument or invalid symbol (see each call) */
+    GB_ENOMEM = -2,        /* device allocation failed                       */
+    GB_ECUDA = -3,         /* CUDA runtime error (message has the details)   */
+    GB_ESTATE = -4,        /* call not allowed in the handle's state         */
+    GB_EUNSUPPORTED = -5   /* shape or device outside what libgb supports    */
+};
+
+/* Retrieval rules. */
+enum {
+    GB_SUM_OF_SUM = 0,     /* Eq.(3)-(5), Alg. 1 */
+    GB_SUM_OF_MAX = 1,     /* Eq.(6)-(7) via bail-out-early (L258-265, L439-483) */
+    GB_HYBRID = 2          /* joint scheme, Alg. 2 (L596-683)                   */
+};
+
+/* Per-probe status written by gb_decode. */
+enum {
+    GB_CONVERGED = 0,      /* V^r == V^{r-1} for some round r <= max_iters     */
+    GB_MAX_ITERS = 1,      /* max_iters rounds ran without a fixed point        */
+    GB_INVALID = 2         /* a probe symbol was >= L (and not GB_ERASED); the
+                              state is all zero and iters is 0                  */
+};
+
+#define GB_ERASED 0xFFFFu
+
+/*
+ * gb_create -- a network of c clusters with l neurons each (PAPER.md L144-145,
+ * "n = CL binary-valued neurons ... grouped into C clusters of L neurons"),
+ * all edges zero (L149), on CUDA device `device`.
+ *   c in [2, 64], l >= 1, n_padded = c*32*ceil(l/32) <= 8192.
+ *   Returns GB_EINVAL for c < 2 or l < 1, GB_EUNSUPPORTED beyond the limits
+ *   or when `device` is not an sm_100 (B200-class) GPU, GB_ENOMEM if W does
+ *   not fit.  *out receives the handle.
+ */
+int gb_create(int c, int l, int device, gb_net **out);
+
+/* gb_destroy -- release W and scratch.  Synchronizes the device.  NULL ok. */
+int gb_destroy(gb_net *net);
+
+/*
+ * gb_clear -- reset W to the empty network (all w_ij = 0) and
+ * the stored count to 0; unseals.  Stream-ordered.
+ */
+int gb_clear(gb_net *net, void *stream);
+
+/*
+ * gb_store -- OR the clique of each of the m messages into W (PAPER.md
+ * L149-153: "we add edges to the network connecting all pairs of nodes
+ * which are activated"; Eq.(1)): for every message and every
+ * cluster pair c != c', w_{(c,m_c)(c',m_c')} = w_{(c',m_c')(c,m_c)} = 1.
+ * msgs: uint16_t[m][c], row-major.  OR is idempotent and commutative, so
+ * calls may come in any order and from any stream split.
+ * A message holding a symbol >= l (GB_ERASED included) stores nothing and
+ * is counted on the device; the count is reported by the next gb_seal.
+ * Unseals the network.  m == 0 is a no-op.  Returns GB_EINVAL for m < 0 or
+ * NULL msgs with m > 0.
+ */
+int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
+
+/*
+ * gb_weights -- expose the library-owned u8 weight matrix W8
+ * (n_padded x n_padded, row-major, W8[i][j] = w_ij in {0,1}, diagonal 0;
+ * gamma is applied at decode, reading R2).  Used for NCCL
+ * broadcast (replicate W) and all-reduce MAX on uint8 (merge sharded
+ * stores: max over {0,1} is OR).  Writing W8 directly unseals nothing by
+ * itself: call gb_seal after modifying it.  *w8 is a device pointer.
+ */
+int gb_weights(gb_net *net, uint8_t **w8, int64_t *nbytes);
+
+/*
+ * gb_seal -- freeze W for retrieval ("At the retrieval stage,
+ * the variables w are fixed"): pack W8 into bit rows (the B200 counterpart of
+ * the compressed W' of L381 / Alg. 2 line 6) and check the structural
+ * invariants w_ij = w_ji (L306) and no intra-cluster or padding edges (L145).
+ * Synchronizes `stream`.  Returns GB_EINVAL if W8 breaks an invariant (the
+ * net stays unsealed) or if a previous gb_store skipped messages with invalid
+ * symbols (the net IS sealed in that case; the message says how many).
+ */
+int gb_seal(gb_net *net, void *stream);
+
+/*
+ * gb_decode -- retrieve k probes in one batch (Eq.(11)
+ * S^t = W V^t: the columns are independent, so results do not depend on the
+ * batch split).
+ *   probes      uint16_t[k][c]; GB_ERASED marks an erased cluster.
+ *   rule        GB_SUM_OF_SUM: V^0 = known one-hot, erased 0 (L197); rounds
+ *                 s = W v + gamma v, keep every per-cluster maximiser (ties
+ *                 all kept; a cluster whose max is 0 activates all its real
+ *                 neurons, readings R3-R4).
+ *               GB_SUM_OF_MAX: V^0 = known one-hot, erased all 1 (L270-271);
+ *                 rounds of Eq.(6)-(7), synchronous.
+ *               GB_HYBRID: Alg. 2 -- one sum-of-sum pass from V^0 (erased 0)
+ *                 keeps erased neurons with exactly C-e signals, then
+ *                 sum-of-max rounds on erased clusters only (known clusters
+ *                 frozen) until the erased clusters stop changing.
+ *   gamma       reinforcement factor (Eq.(3)), 0 <= gamma <= 65535;
+ *               must be > 0 for SUM_OF_MAX / HYBRID (Thm 1), where any
+ *               positive value gives identical results.
+ *   max_iters   maximum number of rounds, 1..65535 (paper runs use 20,
+ *               L700; reading R5).
+ *   out_state   uint32_t[k][c*Wc]   final V (see "decoded state" above)
+ *   out_iters   uint16_t[k]         rounds executed, including the round that
+ *                                   showed no change; hybrid counts only its
+ *                                   sum-of-max rounds (0 when nothing is
+ *                                   erased); reading R6
+ *   out_status  uint8_t[k]          GB_CONVERGED / GB_MAX_ITERS / GB_INVALID
+ * Synchronous rounds (reading R14).  Returns GB_ESTATE if the net is not
+ * sealed, GB_EINVAL for bad rule/gamma/max_iters/k or NULL buffers.
+ * k == 0 is a no-op.
+ */
+int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
+              int max_iters, uint32_t *out_state, uint16_t *out_iters,
+              uint8_t *out_status, void *stream);
+
+/* gb_info -- shape and bookkeeping; any out pointer may be NULL.
+ * stored_count counts messages passed to gb_store since create/clear.      */
+int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count);
+
+/* gb_launch_count -- number of CUDA kernels this handle has launched so far
+ * (diagnostics: bench.py reports the kernels launched in its timed region). */
+int gb_launch_count(gb_net *net, int64_t *launches);
+
+/* gb_last_error -- thread-local message for the last failing call. */
+const char *gb_last_error(void);
+
+/* gb_version -- library version string. */
+const char *gb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GB_H */

@@ -1,0 +1,63 @@
+// gb_internal.h -- private declarations shared by libgb's translation units.
+// Product code only (the oracle never includes this).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gb.h"
+
+namespace gb {
+
+constexpr int kMaxClusters = 64;
+constexpr int kMaxPadded = 8192;      // n_padded limit (W8 = 64 MiB)
+constexpr uint16_t kErased = 0xFFFFu;
+
+// Device-side error bits (gb_net::dflag).
+enum : unsigned {
+    kFlagStoreInvalid = 1u,   // counted separately in dcount[0]
+    kFlagAsym = 2u,           // W8 not symmetric
+    kFlagIntra = 4u,          // edge inside a cluster / on the diagonal
+    kFlagPad = 8u,            // edge touching a padding neuron
+    kFlagNotBinary = 16u      // W8 byte not in {0,1}
+};
+
+struct Shape {
+    int C;      // clusters
+    int L;      // neurons per cluster
+    int Wc;     // 32-bit words per cluster = ceil(L/32)
+    int Lp;     // padded cluster size = 32*Wc
+    int np;     // padded neuron count = C*Lp
+    int nw;     // words per state / per bit row = C*Wc
+};
+
+}  // namespace gb
+
+struct gb_net {
+    gb::Shape s;
+    int device;
+    int sm_count;
+    uint8_t *w8;          // [np][np] u8, row-major
+    uint32_t *wb;         // [np][nw] bit rows
+    unsigned *dflag;      // device error flags
+    unsigned long long *dcount;  // [0] invalid stored messages
+    int64_t stored;
+    bool sealed;
+    // host-staging scratch (gb_decode / gb_store with host pointers)
+    void *stage;
+    size_t stage_bytes;
+    cudaStream_t stage_stream[2];
+    cudaEvent_t stage_event[4];
+    int64_t launches;     // kernels launched by this handle (diagnostics)
+};
+
+namespace gb {
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
+cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
+cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
+                          int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
+                          cudaStream_t st);
+
+}  // namespace gb
