@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""bench.py -- probes decoded/s for the GBNN hybrid rule (arXiv:1303.7032) on B200.
+
+Driver contract (one JSON line from rank 0):
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, NCCL)
+
+A step is one pass of the whole hot path over one batch:
+  gb_clear -> gb_store(this rank's shard of the M messages) -> [N>1: NCCL
+  all-reduce MAX of W8 (uint8)] -> gb_seal -> gb_decode(hybrid, this rank's
+  K probes, device-resident).  Weak scaling: K probes per GPU.
+Default workload = BASELINE config C3: c=8 l=128, M=20000, e=4 erased of 8,
+hybrid rule, gamma=2, max_iters=20, K=10^7 probes per GPU.
+
+`value` is device-timed (CUDA events, max over ranks); `e2e` repeats the step
+through the same C-ABI with pinned HOST buffers (H2D of messages+probes and
+D2H of state/iters/status inside the timed region); `roofline` is measured
+live on the decode kernel; `cpu_baseline` times the CPU oracle on a bounded
+sample on this host (rank 0, N=1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "probes decoded/sec, hybrid rule, c=8 l=128, 1-8 B200; % of TC/HBM roofline"
+RULE_NAMES = {0: "sum-of-sum", 1: "sum-of-max", 2: "hybrid"}
+CONFIGS = {
+    # name: (c, l, M, e, rule, K per GPU, description)
+    "c3": (8, 128, 20000, 4, 2, 10_000_000, "BASELINE C3: c=8 l=128 M=20k e=4 hybrid, 10^7 probes/GPU"),
+    "c2": (8, 128, 5000, 4, 2, 100_000, "BASELINE C2 point: c=8 l=128 M=5k e=4, 10^5 probes"),
+    "c1": (4, 16, 50, 2, 2, 1000, "BASELINE C1: c=4 l=16 M=50 e=2, 1000 probes"),
+    "c4": (16, 256, 100000, 8, 1, 1_000_000, "BASELINE C4: c=16 l=256 M=100k e=8, 10^6 probes"),
+}
+SEED = 0x5EED
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def ncu_traffic(kernel, workload):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    ent = d.get(f"{kernel}|{workload}")
+    return None if ent is None else ent.get("dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling while the timed region runs."""
+    FIELDS = ["timestamp", "clocks.sm", "clocks.max.sm", "power.draw",
+              "clocks_event_reasons.hw_slowdown", "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+        t0 = time.time()
+        while not self.rows and time.time() - t0 < 5:
+            time.sleep(0.02)
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append((time.time(), parts))
+
+    def mark(self):
+        return len(self.rows)
+
+    def stop(self, first):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.06)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        rows = self.rows[first:] or self.rows[-1:]
+        sm = sorted(float(r[1][1]) for r in rows if r[1][1].replace(".", "").isdigit())
+        mx = max((float(r[1][2]) for r in rows if r[1][2].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[1][4 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows), "power_w_max": max((float(r[1][3]) for r in rows
+                                                          if r[1][3].replace(".", "").isdigit()), default=None)}
+
+
+def cpu_oracle_sample(msgs, probes, c, l, rule, gamma, max_iters, budget_s, gpu_out=None, idx0=0):
+    """Time the CPU oracle (as it stands) on a bounded prefix of the workload."""
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    import numpy as np
+    import oracle
+    w, _ = oracle.store(msgs, c, l)
+    cal = min(len(probes), 256)
+    t0 = time.perf_counter()
+    oracle.decode(w, c, l, probes[:cal], rule, gamma=gamma, max_iters=max_iters)
+    rate = cal / max(time.perf_counter() - t0, 1e-6)
+    n = int(min(len(probes), max(cal, rate * budget_s)))
+    t0 = time.perf_counter()
+    st, it, ss = oracle.decode(w, c, l, probes[:n], rule, gamma=gamma, max_iters=max_iters)
+    dt = time.perf_counter() - t0
+    parity = None
+    if gpu_out is not None:
+        gs, gi, gt = gpu_out
+        parity = bool(np.array_equal(gs[:n], st) and np.array_equal(gi[:n], it) and np.array_equal(gt[:n], ss))
+    return n, dt, parity
+
+
+def run_reference(args, cfg):
+    """--impl reference: the CPU oracle, as it stands, on host cores."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import gbgen
+    c, l, m, e, rule, k, desc = cfg
+    msgs = gbgen.messages(SEED, m, c, l)
+    per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    pool = min(k, 200_000)
+    probes, _ = gbgen.probes(SEED + 1, msgs, pool, e, l)
+    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    import oracle
+    w, _ = oracle.store(msgs, c, l)
+    cal = 256
+    t0 = time.perf_counter()
+    oracle.decode(w, c, l, probes[:cal], rule, gamma=args.gamma, max_iters=args.max_iters)
+    rate = cal / (time.perf_counter() - t0)
+    n = int(min(pool, max(cal, rate * per_step)))
+    times = []
+    for s in range(args.warmup + args.steps):
+        off = (s * n) % max(1, pool - n + 1)
+        t0 = time.perf_counter()
+        oracle.store(msgs, c, l)
+        oracle.decode(w, c, l, probes[off:off + n], rule, gamma=args.gamma, max_iters=args.max_iters)
+        if s >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = n * len(times) / tot
+    sample = f"{n} probes/step of {desc} (+ store of all {m} messages each step)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "probes/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+        "data": "synthetic (gbgen splitmix64, seed 0x5EED)",
+        "config": config_dict(args, cfg, ws),
+        "cpu_baseline": {"value": value, "unit": "probes/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "kind": "oracle", "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": "probes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(args, cfg, ws):
+    c, l, m, e, rule, k, desc = cfg
+    return {"workload": desc, "c": c, "l": l, "M": m, "erased": e, "rule": RULE_NAMES[rule],
+            "gamma": args.gamma, "max_iters": args.max_iters, "probes_per_gpu": k,
+            "global_batch": k * ws, "parallelism": f"dp{ws} (probe shards; W merged by NCCL MAX)",
+            "l2": "inputs larger than L2 (probes 16 B + state/iters/status 131 B per probe; "
+                  "1.47 GB per step at K=10^7)",
+            "seed": SEED}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c3", choices=sorted(CONFIGS))
+    ap.add_argument("--rule", type=int, default=None)
+    ap.add_argument("--messages", type=int, default=None)
+    ap.add_argument("--probes", type=int, default=None)
+    ap.add_argument("--gamma", type=int, default=2)
+    ap.add_argument("--max-iters", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    c, l, m, e, rule, k, desc = CONFIGS[args.config]
+    if args.rule is not None:
+        rule = args.rule
+    if args.messages is not None:
+        m = args.messages
+    if args.probes is not None:
+        k = args.probes
+    if (args.rule, args.messages, args.probes) != (None, None, None):
+        desc = f"c={c} l={l} M={m} e={e} {RULE_NAMES[rule]}, {k} probes/GPU"
+    cfg = (c, l, m, e, rule, k, desc)
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import numpy as np
+    import torch
+    import gbgen
+    import paper_1303_7032_b200 as gb
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    msgs = gbgen.messages(SEED, m, c, l)
+    probes, _ = gbgen.probes(SEED + 1, msgs, k, e, l, start=rank * k)
+    my_msgs = np.ascontiguousarray(msgs[rank::ws])
+    msgs_d = torch.from_numpy(my_msgs.view(np.int16)).to(dev)
+    probes_d = torch.from_numpy(probes.view(np.int16)).to(dev)
+    net = gb.Net(c, l, device=local)
+    out = net.alloc_outputs(k, device=True)
+    w8 = net.weights()
+    stream = torch.cuda.current_stream()
+    nw = net.nw
+    t_dec = []
+
+    def step(timed):
+        net.clear()
+        net.store(msgs_d)
+        if dist is not None:
+            dist.all_reduce(w8, op=dist.ReduceOp.MAX)
+        net.seal()
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        net.decode(probes_d, rule, gamma=args.gamma, max_iters=args.max_iters, out=out)
+        if timed:
+            b.record(stream)
+            t_dec.append((a, b))
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    first = sampler.mark()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = net.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(True)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = sampler.stop(first)
+    launches = net.launch_count() - l0
+    ms = ev0.elapsed_time(ev1)
+    dec_ms = sum(a.elapsed_time(b) for a, b in t_dec) / len(t_dec)
+    tm = torch.tensor([ms, dec_ms], device=dev, dtype=torch.float64)
+    if dist is not None:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms, dec_ms = float(tm[0]), float(tm[1])
+    value = ws * k * args.steps / (ms / 1e3)
+
+    # roofline of the dominant kernel (the decode kernel, one launch per call)
+    hbm, _, peak_kind = measured_peaks()
+    bytes_per_probe = 2 * c + 4 * nw + 2 + 1
+    achieved = k * bytes_per_probe / (dec_ms / 1e3) / 1e9
+    kernel = net.decode_kernel(rule)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+            "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
+            "algorithmic_bytes_per_probe": bytes_per_probe, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
+            "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
+
+    # e2e through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        msgs_h = torch.from_numpy(my_msgs.view(np.int16)).pin_memory()
+        probes_h = torch.from_numpy(probes.view(np.int16)).pin_memory()
+        out_h = net.alloc_outputs(k, device=False, pin=True)
+
+        def e2e_step():
+            net.clear()
+            net.store(msgs_h)
+            if dist is not None:
+                dist.all_reduce(w8, op=dist.ReduceOp.MAX)
+            net.seal()
+            net.decode(probes_h, rule, gamma=args.gamma, max_iters=args.max_iters, out=out_h)
+
+        e2e_step()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": ws * k * args.e2e_steps / (float(te[0]) / 1e3), "unit": "probes/s",
+               "h2d_bytes_per_step": int(my_msgs.nbytes + probes.nbytes),
+               "d2h_bytes_per_step": int(k * (4 * nw + 3)),
+               "how": "gb_store + gb_seal + gb_decode with pinned host buffers (library-staged, "
+                      "double-buffered H2D/kernel/D2H)"}
+        ok = (np.array_equal(out_h[0].numpy(), out[0].cpu().numpy()) and
+              np.array_equal(out_h[1].numpy(), out[1].cpu().numpy()))
+        e2e["matches_device_path"] = bool(ok)
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        gs = out[0].cpu().numpy().view(np.uint32)
+        gi = out[1].cpu().numpy().view(np.uint16)
+        gt = out[2].cpu().numpy()
+        n, dt, parity = cpu_oracle_sample(msgs, probes, c, l, rule, args.gamma, args.max_iters,
+                                          args.cpu_budget, (gs, gi, gt))
+        cpu = {"value": n / dt, "unit": "probes/s", "cores": int(os.environ.get("OMP_NUM_THREADS", host_cores())),
+               "kind": "oracle", "sample": f"first {n} probes of the same batch ({desc}), W from the same "
+                                           f"{m} messages; {dt:.1f} s", "cpu": cpu_model(),
+               "parity_vs_gpu_on_sample": parity}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "probes/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "data": "synthetic (gbgen splitmix64, seed 0x5EED; iid uniform symbols, uniform erasures)",
+                "config": config_dict(args, cfg, ws), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    net.close()
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

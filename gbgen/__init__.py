@@ -69,31 +69,45 @@ def erasure_masks(seed: int, k: int, c: int, e, start: int = 0) -> np.ndarray:
     if k and (e_arr.min() < 0 or e_arr.max() > c):
         raise ValueError("erasure count must lie in [0, C]")
     perm = np.broadcast_to(np.arange(c, dtype=np.int64), (k, c)).copy()
-    rows = np.arange(k)
+    flat = perm.reshape(-1)
+    base = np.arange(k, dtype=np.int64) * c
     emax = int(e_arr.max()) if k else 0
-    if emax:
-        x = stream(seed, 2, (start) * c, k * c).reshape(k, c)
+    uniform = bool(k) and int(e_arr.min()) == emax
+    ctr = (np.arange(start, start + k, dtype=np.uint64) * np.uint64(c)) if emax else None
+    sbase = np.uint64((seed ^ (2 << 56)) & 0xFFFFFFFFFFFFFFFF)
     for j in range(emax):
-        r = (x[:, j] % np.uint64(c - j)).astype(np.int64)
-        a = perm[rows, j].copy()
-        b = perm[rows, j + r].copy()
-        act = j < e_arr
-        perm[rows[act], j] = b[act]
-        perm[rows[act], (j + r)[act]] = a[act]
+        xj = splitmix64(sbase ^ (ctr + np.uint64(j)))          # x_{seed,2,k*C+j}
+        r = (xj % np.uint64(c - j)).astype(np.int64)
+        src = base + j + r
+        a = flat[base + j].copy()
+        b = flat[src]
+        if uniform:
+            flat[base + j] = b
+            flat[src] = a
+        else:
+            act = j < e_arr
+            flat[(base + j)[act]] = b[act]
+            flat[src[act]] = a[act]
     mask = np.zeros((k, c), dtype=bool)
+    mflat = mask.reshape(-1)
     for j in range(emax):
-        act = j < e_arr
-        mask[rows[act], perm[act, j]] = True
+        if uniform:
+            mflat[base + perm[:, j]] = True
+        else:
+            act = j < e_arr
+            mflat[(base + perm[:, j])[act]] = True
     return mask
 
 
 def probes(seed: int, msgs: np.ndarray, k: int, e, l: int,
-           random_count: int = 0):
+           random_count: int = 0, start: int = 0):
     """K probes: stored messages (with replacement) with e clusters erased.
 
     The last ``random_count`` probes are random non-stored words (stream 3)
-    erased the same way.  Returns (probes uint16 [K, C], source int64 [K];
-    source = -1 for random probes).
+    erased the same way.  ``start`` offsets the global probe counter, so a
+    shard [start, start+K) of a larger batch is generated identically on any
+    rank.  Returns (probes uint16 [K, C], source int64 [K]; source = -1 for
+    random probes).
     """
     m, c = msgs.shape
     if k and m == 0 and random_count < k:
@@ -110,15 +124,15 @@ def probes(seed: int, msgs: np.ndarray, k: int, e, l: int,
         sblk = np.full(n, -1, dtype=np.int64)
         if stored.any():
             ns = int(stored.sum())
-            pick = (stream(seed, 1, s, ns) % np.uint64(m)).astype(np.int64)
+            pick = (stream(seed, 1, start + s, ns) % np.uint64(m)).astype(np.int64)
             blk[:ns] = msgs[pick]
             sblk[:ns] = pick
         if (~stored).any():
             nr = int((~stored).sum())
-            r0 = s + n - nr
+            r0 = start + s + n - nr
             sym = stream(seed, 3, r0 * c, nr * c) % np.uint64(l)
             blk[n - nr:] = sym.astype(np.uint16).reshape(nr, c)
-        mask = erasure_masks(seed, n, c, e_arr[s:s + n], start=s)
+        mask = erasure_masks(seed, n, c, e_arr[s:s + n], start=start + s)
         blk[mask] = ERASED
         out[s:s + n] = blk
         src[s:s + n] = sblk

@@ -164,6 +164,10 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count);
  * (diagnostics: bench.py reports the kernels launched in its timed region). */
 int gb_launch_count(gb_net *net, int64_t *launches);
 
+/* gb_decode_kernel -- name of the kernel gb_decode launches for `rule` on
+ * this handle's shape (diagnostics for profiling and roofline reports). */
+const char *gb_decode_kernel(gb_net *net, int rule);
+
 /* gb_last_error -- thread-local message for the last failing call. */
 const char *gb_last_error(void);
 

@@ -29,7 +29,8 @@ LIB_PATH = os.path.join(_HERE, "libgb.so")
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_seal",
-           "gb_decode", "gb_info", "gb_launch_count", "gb_last_error", "gb_version")
+           "gb_decode", "gb_info", "gb_launch_count", "gb_decode_kernel", "gb_last_error",
+           "gb_version")
 
 _lib = None
 
@@ -61,6 +62,7 @@ def lib() -> ctypes.CDLL:
         "gb_info": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                      ctypes.POINTER(i64)], i32),
         "gb_launch_count": ([P, ctypes.POINTER(i64)], i32),
+        "gb_decode_kernel": ([P, i32], ctypes.c_char_p),
         "gb_last_error": ([], ctypes.c_char_p),
         "gb_version": ([], ctypes.c_char_p),
     }
@@ -157,6 +159,9 @@ class Net:
         n = ctypes.c_int64()
         _check(lib().gb_launch_count(self._h, ctypes.byref(n)))
         return n.value
+
+    def decode_kernel(self, rule: int) -> str:
+        return lib().gb_decode_kernel(self._h, rule).decode()
 
     def alloc_outputs(self, k: int, device: bool = True, pin: bool = False):
         import torch

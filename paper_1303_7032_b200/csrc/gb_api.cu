@@ -12,6 +12,8 @@
 #include "gb_internal.h"
 
 namespace gb {
+cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                               uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k, int rule,
                                   int gamma, int max_iters, uint32_t *state, uint16_t *iters,
                                   uint8_t *status, cudaStream_t st);
@@ -309,6 +311,14 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
     return GB_OK;
 }
 
+const char *gb_decode_kernel(gb_net *net, int rule) {
+    if (!net) return "";
+    const gb::Shape &s = net->s;
+    if (rule != GB_SUM_OF_SUM && s.C <= 8 && s.np <= 1024 && (s.Wc == 1 || s.Wc == 2 || s.Wc == 4))
+        return "decode_smem_kernel";
+    return "decode_generic_kernel";
+}
+
 int gb_launch_count(gb_net *net, int64_t *launches) {
     if (!net || !launches) return fail(GB_EINVAL, "gb_launch_count: NULL argument");
     *launches = net->launches;
@@ -323,6 +333,8 @@ namespace gb {
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st) {
+    cudaError_t e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
+    if (e != cudaErrorNotSupported) return e;
     return launch_decode_generic(net, probes, k, rule, gamma, max_iters, state, iters, status, st);
 }
 
