@@ -313,9 +313,7 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
-    const gb::Shape &s = net->s;
-    if (rule != GB_SUM_OF_SUM && s.C <= 8 && s.np <= 1024 && (s.Wc == 1 || s.Wc == 2 || s.Wc == 4))
-        return "decode_smem_kernel";
+    if (gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     return "decode_generic_kernel";
 }
 

@@ -3,13 +3,16 @@
 // (hybrid rule, c=8 l=128).
 //
 // Layout (DESIGN.md §Kernels / "smem bit kernel"):
-//  * W bit rows Wb[np][nw] copied once per CTA into shared memory (128 KiB at
-//    c=8 l=128); block c of row j = words [c*WC, c*WC+WC).
+//  * W bit rows copied once per CTA into shared memory (128 KiB at c=8
+//    l=128).  Row j holds C blocks of WC words; block c of row j is stored
+//    at block slot (c ^ (j & m)), m = C-1 for power-of-two C (else 0), so
+//    the rows that different lanes read land in different bank groups.
 //  * one thread = one probe.  The probe's in-scope cluster states X[t][WC]
 //    (t indexes the slot list: erased clusters for the hybrid, all clusters
-//    for sum-of-max) live in a per-thread shared-memory area, two buffers
-//    (synchronous rounds), interleaved [word][thread] so accesses are
-//    bank-conflict free.
+//    for sum-of-max) live in a per-thread shared-memory area laid out
+//    [word][thread] (bank-conflict free); the next state of each slot is
+//    built in registers (static slot unroll) and written back after the
+//    round, so rounds are synchronous.
 //
 // Method:
 //  a1 ingest  -- probe symbols -> erased list; symbol >= L -> GB_INVALID.
@@ -20,40 +23,36 @@
 //  a6 round   -- Eq.(6)-(7) by bail-out-early (Thm 1) in "push"
 //                form: for target slot t and every other source slot s,
 //                H = OR of block c_t of the rows j in X_s, accumulated until
-//                H covers the still-alive part of X_t (the first time a
-//                candidate receives a signal from cluster c_s is enough,
-//                L449); alive &= H; a target found dead in one source cluster
-//                stops being walked (L450).  Dead neurons stay dead (Lemma 1).
-//                Hybrid: targets and sources are the erased clusters only;
-//                known clusters are frozen one-hot (Alg. 2) and
-//                every candidate is adjacent to them by the prune.
+//                H covers the still-alive part of X_t (the first signal a
+//                candidate receives from cluster c_s is enough, L449);
+//                alive &= H; a target found dead stops being walked (L450).
+//                Dead neurons stay dead (Lemma 1).  Hybrid: targets and
+//                sources are the erased clusters only; known clusters are
+//                frozen one-hot (Alg. 2) and every candidate is
+//                adjacent to them by the prune.
 //  a7 output  -- state bits, rounds (incl. the confirming round), status.
 #include "gb_internal.h"
 
 namespace gb {
 namespace {
 
-constexpr int kSmemThreads = 256;
+constexpr int kSmemThreads = 768;
 constexpr int kMaxC = 8;
 
 template <int WC>
-__device__ __forceinline__ void load_block(const uint32_t *p, uint32_t (&v)[WC]) {
+__device__ __forceinline__ void lds_block(uint32_t addr, uint32_t (&v)[WC]) {
     if constexpr (WC == 4) {
-        const uint4 q = *reinterpret_cast<const uint4 *>(p);
-        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]) : "r"(addr));
     } else if constexpr (WC == 2) {
-        const uint2 q = *reinterpret_cast<const uint2 *>(p);
-        v[0] = q.x; v[1] = q.y;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(addr));
     } else {
-#pragma unroll
-        for (int u = 0; u < WC; ++u) v[u] = p[u];
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v[0]) : "r"(addr));
     }
 }
 
-template <int WC>
 __device__ __forceinline__ uint32_t real_mask_u(int L, int u) {
-    const int lo = u * 32;
-    const int nb = min(32, max(0, L - lo));
+    const int nb = min(32, max(0, L - u * 32));
     return nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
 }
 
@@ -64,20 +63,23 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                    uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int LP = 32 * WC;
+    constexpr int BB = 4 * WC;                      // bytes per block
     const int C = s.C;
     const int nw = C * WC;
     const int np = C * LP;
-    uint32_t *W = smem;                                  // [np][nw]
-    uint32_t *XA = smem + np * nw;                       // [C*WC][threads]
-    uint32_t *XB = XA + kMaxC * WC * kSmemThreads;
+    const int rowB = nw * 4;                        // bytes per row
+    const uint32_t swz = ((C & (C - 1)) == 0) ? (uint32_t)(C - 1) : 0u;
+    uint32_t *W = smem;
+    uint32_t *X = smem + np * nw;                   // [kMaxC*WC][threads]
     const int tid = threadIdx.x;
+    const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
 
-    // W -> shared memory, 16 B per thread per step.
-    {
-        const int n16 = np * nw / 4;
-        const uint4 *src = reinterpret_cast<const uint4 *>(wb);
-        uint4 *dst = reinterpret_cast<uint4 *>(W);
-        for (int i = tid; i < n16; i += kSmemThreads) dst[i] = __ldg(src + i);
+    // W -> shared memory with the block swizzle.
+    for (int i = tid; i < np * C; i += kSmemThreads) {
+        const int j = i / C, c = i - j * C;
+        const int pc = c ^ (int)(j & swz);
+#pragma unroll
+        for (int u = 0; u < WC; ++u) W[j * nw + pc * WC + u] = __ldg(wb + (int64_t)j * nw + c * WC + u);
     }
     __syncthreads();
 
@@ -86,8 +88,14 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         // ---- a1 ingest
         unsigned sym[kMaxC];
         const uint16_t *pr = probes + p * C;
+        if (C == 8) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4 *>(pr));
+            sym[0] = q.x & 0xffffu; sym[1] = q.x >> 16; sym[2] = q.y & 0xffffu; sym[3] = q.y >> 16;
+            sym[4] = q.z & 0xffffu; sym[5] = q.z >> 16; sym[6] = q.w & 0xffffu; sym[7] = q.w >> 16;
+        } else {
 #pragma unroll
-        for (int c = 0; c < kMaxC; ++c) sym[c] = (c < C) ? (unsigned)__ldg(pr + c) : 0u;
+            for (int c = 0; c < kMaxC; ++c) sym[c] = (c < C) ? (unsigned)__ldg(pr + c) : 0u;
+        }
         unsigned emask = 0, bad = 0;
 #pragma unroll
         for (int c = 0; c < kMaxC; ++c) {
@@ -112,31 +120,35 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 ++nslot;
             }
         }
-        uint32_t *X = XA, *Xn = XB;
-        // ---- a5 prune / init
-        for (unsigned t = 0; t < nslot; ++t) {
-            const int c = (slots >> (4 * t)) & 15;
-            uint32_t x[WC];
-            if ((emask >> c) & 1u) {
+        // ---- a5 prune / init -> X  (static cluster loop; slot = rank in scope mask)
+        const unsigned scope = (RULE == GB_SUM_OF_MAX) ? ((1u << C) - 1u) : emask;
 #pragma unroll
-                for (int u = 0; u < WC; ++u) x[u] = real_mask_u<WC>(s.L, u);
-                if (RULE == GB_HYBRID) {
+        for (int c = 0; c < kMaxC; ++c) {
+            if (c < C && ((scope >> c) & 1u)) {
+                const int t = __popc(scope & ((1u << c) - 1u));
+                uint32_t x[WC];
+                if ((emask >> c) & 1u) {
 #pragma unroll
-                    for (int kc = 0; kc < kMaxC; ++kc) {
-                        if (kc < C && !((emask >> kc) & 1u)) {
-                            uint32_t r[WC];
-                            load_block<WC>(W + (kc * LP + sym[kc]) * nw + c * WC, r);
+                    for (int u = 0; u < WC; ++u) x[u] = real_mask_u(s.L, u);
+                    if (RULE == GB_HYBRID) {
 #pragma unroll
-                            for (int u = 0; u < WC; ++u) x[u] &= r[u];
+                        for (int kc = 0; kc < kMaxC; ++kc) {
+                            if (kc < C && !((emask >> kc) & 1u)) {
+                                uint32_t r[WC];
+                                const uint32_t pc = (uint32_t)c ^ (sym[kc] & swz);
+                                lds_block<WC>(w_s + (uint32_t)(kc * LP + sym[kc]) * rowB + pc * BB, r);
+#pragma unroll
+                                for (int u = 0; u < WC; ++u) x[u] &= r[u];
+                            }
                         }
                     }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) x[u] = ((int)(sym[c] >> 5) == u) ? (1u << (sym[c] & 31)) : 0u;
                 }
-            } else {
 #pragma unroll
-                for (int u = 0; u < WC; ++u) x[u] = ((int)(sym[c] >> 5) == u) ? (1u << (sym[c] & 31)) : 0u;
+                for (int u = 0; u < WC; ++u) X[(t * WC + u) * kSmemThreads + tid] = x[u];
             }
-#pragma unroll
-            for (int u = 0; u < WC; ++u) X[(t * WC + u) * kSmemThreads + tid] = x[u];
         }
 
         int it = 0;
@@ -146,57 +158,68 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         } else {
             // ---- a6 rounds
             while (it < T) {
+                uint32_t xn[kMaxC][WC];
                 bool changed = false;
-                for (unsigned t = 0; t < nslot; ++t) {
-                    const int c = (slots >> (4 * t)) & 15;
-                    uint32_t x[WC], alive[WC];
 #pragma unroll
-                    for (int u = 0; u < WC; ++u) {
-                        x[u] = X[(t * WC + u) * kSmemThreads + tid];
-                        alive[u] = x[u];
-                    }
-                    uint32_t any = 0;
+                for (int t = 0; t < kMaxC; ++t) {
+                    if (t < (int)nslot) {
+                        const int c = (slots >> (4 * t)) & 15;
+                        uint32_t alive[WC];
+                        uint32_t any = 0;
 #pragma unroll
-                    for (int u = 0; u < WC; ++u) any |= alive[u];
-                    for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
-                        if (sidx == t) continue;
-                        const int c2 = (slots >> (4 * sidx)) & 15;
-                        uint32_t h[WC];
+                        for (int u = 0; u < WC; ++u) {
+                            alive[u] = X[(t * WC + u) * kSmemThreads + tid];
+                            any |= alive[u];
+                        }
+                        for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
+                            if ((int)sidx == t) continue;
+                            const int c2 = (slots >> (4 * sidx)) & 15;
+                            uint32_t w4[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-                        for (int u = 0; u < WC; ++u) h[u] = 0u;
-                        bool covered = false;
+                            for (int u = 0; u < WC; ++u) w4[u] = X[(sidx * WC + u) * kSmemThreads + tid];
+                            uint64_t lo = (uint64_t)w4[0] | ((uint64_t)w4[1] << 32);
+                            uint64_t hi = (uint64_t)w4[2] | ((uint64_t)w4[3] << 32);
+                            // row j = c2*LP + b; address = base + b*rowB + ((c ^ (b & swz)) * BB)
+                            const uint32_t base = w_s + (uint32_t)(c2 * LP) * rowB;
+                            uint32_t h[WC];
 #pragma unroll
-                        for (int u2 = 0; u2 < WC; ++u2) {
-                            uint32_t bits = X[(sidx * WC + u2) * kSmemThreads + tid];
-                            while (bits && !covered) {
-                                const int b = __ffs(bits) - 1;
-                                bits &= bits - 1u;
-                                const int j = c2 * LP + u2 * 32 + b;
+                            for (int u = 0; u < WC; ++u) h[u] = 0u;
+                            uint32_t miss = any;
+                            while ((lo | hi) && miss) {
+                                int b;
+                                if (lo) { b = __ffsll((long long)lo) - 1; lo &= lo - 1; }
+                                else { b = 64 + __ffsll((long long)hi) - 1; hi &= hi - 1; }
                                 uint32_t r[WC];
-                                load_block<WC>(W + j * nw + c * WC, r);
-                                uint32_t miss = 0;
+                                lds_block<WC>(base + (uint32_t)b * rowB + (((uint32_t)c ^ ((uint32_t)b & swz)) * BB), r);
+                                miss = 0u;
 #pragma unroll
                                 for (int u = 0; u < WC; ++u) {
                                     h[u] |= r[u];
                                     miss |= alive[u] & ~h[u];
                                 }
-                                covered = (miss == 0u);
+                            }
+                            any = 0u;
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                alive[u] &= h[u];
+                                any |= alive[u];
                             }
                         }
-                        any = 0;
 #pragma unroll
-                        for (int u = 0; u < WC; ++u) {
-                            alive[u] &= h[u];
-                            any |= alive[u];
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < WC; ++u) {
-                        Xn[(t * WC + u) * kSmemThreads + tid] = alive[u];
-                        changed |= (alive[u] != x[u]);
+                        for (int u = 0; u < WC; ++u) xn[t][u] = alive[u];
                     }
                 }
-                uint32_t *tmp = X; X = Xn; Xn = tmp;
+#pragma unroll
+                for (int t = 0; t < kMaxC; ++t) {
+                    if (t < (int)nslot) {
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) {
+                            uint32_t *a = &X[(t * WC + u) * kSmemThreads + tid];
+                            changed |= (*a != xn[t][u]);
+                            *a = xn[t][u];
+                        }
+                    }
+                }
                 ++it;
                 if (!changed) { status = GB_CONVERGED; break; }
             }
@@ -225,11 +248,15 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     }
 }
 
+size_t smem_bytes(const Shape &s, int wc) {
+    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4;
+}
+
 template <int WC, int RULE>
 cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                      uint16_t *iters, uint8_t *status, cudaStream_t st) {
     const Shape &s = net->s;
-    const size_t smem = (size_t)s.np * s.nw * 4 + 2ull * kMaxC * WC * kSmemThreads * 4;
+    const size_t smem = smem_bytes(s, WC);
     auto fn = decode_smem_kernel<WC, RULE>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -242,22 +269,25 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
 
 }  // namespace
 
+bool decode_smem_supported(const Shape &s, int rule) {
+    if (s.C > kMaxC || s.np > 1024 || rule == GB_SUM_OF_SUM) return false;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4) return false;
+    return smem_bytes(s, s.Wc) <= 227 * 1024;
+}
+
 // Returns cudaErrorNotSupported when the shape does not fit this kernel.
 cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
                                uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     const Shape &s = net->s;
-    if (s.C > kMaxC || s.np > 1024 || rule == GB_SUM_OF_SUM) return cudaErrorNotSupported;
-    const size_t smem = (size_t)s.np * s.nw * 4 + 2ull * kMaxC * s.Wc * kSmemThreads * 4;
-    if (smem > 227 * 1024) return cudaErrorNotSupported;
+    if (!decode_smem_supported(s, rule)) return cudaErrorNotSupported;
     const bool hyb = (rule == GB_HYBRID);
     switch (s.Wc) {
         case 1: return hyb ? launch_t<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
                            : launch_t<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
         case 2: return hyb ? launch_t<2, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
                            : launch_t<2, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 4: return hyb ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                           : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        default: return cudaErrorNotSupported;
+        default: return hyb ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
+                            : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
     }
 }
 

@@ -56,6 +56,7 @@ namespace gb {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
+bool decode_smem_supported(const Shape &s, int rule);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st);
