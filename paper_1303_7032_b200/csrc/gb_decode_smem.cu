@@ -71,8 +71,11 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     const uint32_t swz = ((C & (C - 1)) == 0) ? (uint32_t)(C - 1) : 0u;
     uint32_t *W = smem;
     uint32_t *X = smem + np * nw;                   // [kMaxC*WC][threads]
+    uint32_t *Z = X + kMaxC * WC * kSmemThreads;    // one all-zero block
     const int tid = threadIdx.x;
     const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
+    const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(Z);
+    if (tid < 4) Z[tid] = 0u;
 
     // W -> shared memory with the block swizzle.
     for (int i = tid; i < np * C; i += kSmemThreads) {
@@ -174,28 +177,33 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                         for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
                             if ((int)sidx == t) continue;
                             const int c2 = (slots >> (4 * sidx)) & 15;
-                            uint32_t w4[4] = {0u, 0u, 0u, 0u};
-#pragma unroll
-                            for (int u = 0; u < WC; ++u) w4[u] = X[(sidx * WC + u) * kSmemThreads + tid];
-                            uint64_t lo = (uint64_t)w4[0] | ((uint64_t)w4[1] << 32);
-                            uint64_t hi = (uint64_t)w4[2] | ((uint64_t)w4[3] << 32);
-                            // row j = c2*LP + b; address = base + b*rowB + ((c ^ (b & swz)) * BB)
-                            const uint32_t base = w_s + (uint32_t)(c2 * LP) * rowB;
                             uint32_t h[WC];
 #pragma unroll
                             for (int u = 0; u < WC; ++u) h[u] = 0u;
                             uint32_t miss = any;
-                            while ((lo | hi) && miss) {
-                                int b;
-                                if (lo) { b = __ffsll((long long)lo) - 1; lo &= lo - 1; }
-                                else { b = 64 + __ffsll((long long)hi) - 1; hi &= hi - 1; }
-                                uint32_t r[WC];
-                                lds_block<WC>(base + (uint32_t)b * rowB + (((uint32_t)c ^ ((uint32_t)b & swz)) * BB), r);
-                                miss = 0u;
+                            const uint32_t ckey = (uint32_t)c;
 #pragma unroll
-                                for (int u = 0; u < WC; ++u) {
-                                    h[u] |= r[u];
-                                    miss |= alive[u] & ~h[u];
+                            for (int u2 = 0; u2 < WC; ++u2) {
+                                uint32_t cur = X[(sidx * WC + u2) * kSmemThreads + tid];
+                                // row j = c2*LP + u2*32 + b  ->  j & swz == b & swz
+                                const uint32_t base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
+                                while (cur && miss) {
+                                    // two rows per check: the second is the zero block when
+                                    // only one candidate is left (branch-free, ILP 2)
+                                    const uint32_t b1 = __ffs(cur) - 1;
+                                    cur &= cur - 1u;
+                                    const uint32_t b2 = __ffs(cur) - 1;
+                                    cur &= cur - 1u;
+                                    uint32_t r[WC], r2[WC];
+                                    lds_block<WC>(base + b1 * rowB + ((ckey ^ (b1 & swz)) * BB), r);
+                                    const uint32_t a2 = base + b2 * rowB + ((ckey ^ (b2 & swz)) * BB);
+                                    lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
+                                    miss = 0u;
+#pragma unroll
+                                    for (int u = 0; u < WC; ++u) {
+                                        h[u] |= r[u] | r2[u];
+                                        miss |= alive[u] & ~h[u];
+                                    }
                                 }
                             }
                             any = 0u;
@@ -249,7 +257,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
 }
 
 size_t smem_bytes(const Shape &s, int wc) {
-    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4;
+    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4 + 16;
 }
 
 template <int WC, int RULE>
