@@ -123,31 +123,54 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 ++nslot;
             }
         }
-        // ---- a5 prune / init -> X  (static cluster loop; slot = rank in scope mask)
-        const unsigned scope = (RULE == GB_SUM_OF_MAX) ? ((1u << C) - 1u) : emask;
+        // ---- a5 prune / init -> X.  Slots are a static unroll (their count is
+        // uniform across a warp when e is); the known clusters are walked in a
+        // dynamic loop of C-e trips, one bit row per known neuron.
+        uint64_t sp_lo = 0, sp_hi = 0;   // symbols packed 16 bits per cluster
 #pragma unroll
         for (int c = 0; c < kMaxC; ++c) {
-            if (c < C && ((scope >> c) & 1u)) {
-                const int t = __popc(scope & ((1u << c) - 1u));
+            if (c < 4) sp_lo |= (uint64_t)(sym[c] & 0xffffu) << (16 * c);
+            else sp_hi |= (uint64_t)(sym[c] & 0xffffu) << (16 * (c - 4));
+        }
+        // known rows: ra[kk] = smem address of row (kc, p_kc), rk[kk] = its swizzle key * BB
+        uint32_t ra[kMaxC], rk[kMaxC];
+        unsigned nk = 0;
+        if (RULE == GB_HYBRID) {
+            unsigned km = (~emask) & ((1u << C) - 1u);
+            nk = __popc(km);
+#pragma unroll
+            for (int kk = 0; kk < kMaxC; ++kk) {
+                const unsigned kc = __ffs(km) - 1;
+                km &= km - 1u;
+                const unsigned sk = (unsigned)(((kc < 4) ? sp_lo : sp_hi) >> (16 * (kc & 3))) & 0xffffu;
+                ra[kk] = w_s + (kc * LP + sk) * rowB;
+                rk[kk] = (sk & swz) * BB;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kMaxC; ++t) {
+            if (t < (int)nslot) {
+                const unsigned c = (slots >> (4 * t)) & 15u;
                 uint32_t x[WC];
                 if ((emask >> c) & 1u) {
 #pragma unroll
                     for (int u = 0; u < WC; ++u) x[u] = real_mask_u(s.L, u);
                     if (RULE == GB_HYBRID) {
+                        const uint32_t cb = c * BB;
 #pragma unroll
-                        for (int kc = 0; kc < kMaxC; ++kc) {
-                            if (kc < C && !((emask >> kc) & 1u)) {
+                        for (int kk = 0; kk < kMaxC; ++kk) {
+                            if (kk < (int)nk) {
                                 uint32_t r[WC];
-                                const uint32_t pc = (uint32_t)c ^ (sym[kc] & swz);
-                                lds_block<WC>(w_s + (uint32_t)(kc * LP + sym[kc]) * rowB + pc * BB, r);
+                                lds_block<WC>(ra[kk] + (cb ^ rk[kk]), r);
 #pragma unroll
                                 for (int u = 0; u < WC; ++u) x[u] &= r[u];
                             }
                         }
                     }
                 } else {
+                    const unsigned sc = (unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 0xffffu;
 #pragma unroll
-                    for (int u = 0; u < WC; ++u) x[u] = ((int)(sym[c] >> 5) == u) ? (1u << (sym[c] & 31)) : 0u;
+                    for (int u = 0; u < WC; ++u) x[u] = ((sc >> 5) == (unsigned)u) ? (1u << (sc & 31)) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < WC; ++u) X[(t * WC + u) * kSmemThreads + tid] = x[u];
@@ -243,7 +266,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
 #pragma unroll
             for (int u = 0; u < WC; ++u)
                 v[u] = so ? X[((so - 1) * WC + u) * kSmemThreads + tid]
-                          : (((int)(sym[c] >> 5) == u) ? (1u << (sym[c] & 31)) : 0u);
+                          : ((((unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 0xffffu) >> 5) == (unsigned)u
+                                 ? (1u << ((unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 31u)) : 0u);
             if constexpr (WC == 4) {
                 *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
             } else {
