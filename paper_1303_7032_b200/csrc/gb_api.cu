@@ -138,6 +138,7 @@ int gb_create(int c, int l, int device, gb_net **out) {
         gb_destroy(net);
         return cuda_fail(e, "gb_create: init");
     }
+    gb::sos_tc_make_map(net);   // TMA descriptor of W8 for the tensor-core SOS kernel
     *out = net;
     return GB_OK;
 }
@@ -313,7 +314,8 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
-    if (gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
+    if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
+    if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     return "decode_generic_kernel";
 }
 
@@ -331,7 +333,13 @@ namespace gb {
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st) {
-    cudaError_t e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
+    cudaError_t e = cudaErrorNotSupported;
+    if (rule == GB_SUM_OF_SUM) {
+        if (net->wmap_ok && sos_tc_supported(net->s))
+            e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, state, iters, status, st);
+    } else {
+        e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
+    }
     if (e != cudaErrorNotSupported) return e;
     return launch_decode_generic(net, probes, k, rule, gamma, max_iters, state, iters, status, st);
 }

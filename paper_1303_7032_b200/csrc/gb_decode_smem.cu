@@ -207,6 +207,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             const uint32_t ckey = (uint32_t)c;
 #pragma unroll
                             for (int u2 = 0; u2 < WC; ++u2) {
+                                if (!miss) break;
                                 uint32_t cur = X[(sidx * WC + u2) * kSmemThreads + tid];
                                 // row j = c2*LP + u2*32 + b  ->  j & swz == b & swz
                                 const uint32_t base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;

@@ -1,0 +1,415 @@
+// gb_decode_sos_tc.cu -- sum-of-sum decode on the 5th-generation tensor cores.
+//
+// a3 SOS score (Eq.(3), Eq.(10)-(11) L328/L349, Alg. 1 line 4):
+//     S^t = W V^t + gamma V^t
+// is an exact integer contraction: V (0/1) and W (0/1) as uint8, products and
+// sums in int32 -- tcgen05.mma.kind::i8 with the accumulator in TMEM.  One CTA
+// owns a tile of 128 probes (UMMA M = 128, TMEM lane = probe):
+//     D[probe, neuron] = sum_j A[probe, j] * B[neuron, j],  A = V^T,  B = W
+// (W is symmetric, so its rows are the K-major B operand).  W tiles are TMA
+// loaded (128-byte swizzle, K block = 128) from the u8 W8 matrix, double
+// buffered against the MMAs; the A tile is expanded from the state bits into
+// the same swizzled layout by the CTA's threads.
+// a4 WTA + convergence (Eq.(4)-(5) L220-225, Alg. 1): the epilogue
+// reads each probe's TMEM row (tcgen05.ld), adds gamma*v_i, takes the max over
+// each cluster's real neurons and keeps every neuron that reaches it (ties
+// kept, reading R3; max 0 activates all real neurons, R4); the new state bits
+// go back to shared memory and feed the next round's A tile.  Per-probe
+// convergence (V^{t+1} == V^t) and rounds are tracked in registers; the tile
+// iterates until all its probes converged or max_iters rounds ran.  There is
+// no host round-trip between rounds.
+//
+// Passes: TMEM holds 512 int32 columns per lane, so the n_p output columns are
+// processed in passes of NP <= 512 columns made of whole clusters (Lp <= 256;
+// MMA N <= 256 per instruction).
+#include <cuda.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "gb_internal.h"
+
+namespace gb {
+namespace {
+
+constexpr int kTM = 128;       // probes per tile = UMMA M
+constexpr int kKB = 128;       // K bytes per block = one 128 B swizzle atom
+constexpr int kThreads = 128;  // one thread per probe / TMEM lane
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+        ::"r"(dst), "l"((uint64_t)map), "r"(bar), "r"(x), "r"(y) : "memory");
+}
+// UMMA shared-memory descriptor, K-major, 128-byte swizzle: 8-row groups 1024 B apart.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
+           ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+// Instruction descriptor: kind::i8, D = s32, A = B = u8, both K-major, M = 128, N.
+__device__ __forceinline__ uint32_t i8_idesc(int n) {
+    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 4 state bits -> 4 bytes of 0/1 (bit i -> byte i).
+__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
+
+__device__ __forceinline__ uint32_t real_mask(int L, int u) {
+    const int nb = min(32, max(0, L - u * 32));
+    return nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+}
+
+struct SosParams {
+    int NP;        // columns per pass (multiple of Lp, <= 512)
+    int BR;        // TMA box rows (divides Lp, <= 256)
+    uint32_t a_off, b_off, v_off, bar_off;   // shared-memory carve (bytes from the aligned base)
+    uint32_t b_stage;                        // bytes per B stage
+};
+
+template <int WC>
+__global__ void __launch_bounds__(kThreads, 1)
+sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
+              const uint16_t *__restrict__ probes, int64_t k, int gamma, int T,
+              uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
+              uint8_t *__restrict__ out_status) {
+    constexpr int LP = 32 * WC;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t A0 = base + P.a_off;                 // 2 stages x (128 x 128 B)
+    const uint32_t B0 = base + P.b_off;                 // 2 stages x (NP x 128 B)
+    uint32_t *Vs = reinterpret_cast<uint32_t *>(gbase + P.v_off);   // [nw][128] x 2 buffers
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
+    const uint32_t tma_bar0 = smem_u32(&bars[0]), mma_bar0 = smem_u32(&bars[2]);
+
+    const int m = threadIdx.x;
+    const int warp = m >> 5;
+    const int nw = s.nw, np = s.np;
+    const int nkb = (np + kKB - 1) / kKB;
+    const int npass = (np + P.NP - 1) / P.NP;
+
+    if (m == 0) {
+        mbar_init(tma_bar0, 1);
+        mbar_init(tma_bar0 + 8, 1);
+        mbar_init(mma_bar0, 1);
+        mbar_init(mma_bar0 + 8, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&wmap) : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t tmem_lane = tmem + ((uint32_t)(warp * 32) << 16);
+
+    uint32_t it_count = 0;   // K-block iterations issued so far (stage/phase bookkeeping)
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p = tile * kTM + m;
+        uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+        // ---- a1 ingest: V^0 = known one-hot, erased clusters 0
+        bool done = true;   // converged, invalid or beyond k
+        int status = GB_MAX_ITERS, iters = 0;
+        bool valid = false;
+        if (p < k) {
+            valid = true;
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+            }
+            done = !valid;
+            if (!valid) status = GB_INVALID;
+        }
+        for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
+        if (valid) {
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
+            }
+        }
+        __syncthreads();
+
+        for (int r = 1; r <= T; ++r) {
+            if (__syncthreads_and(done)) break;
+            // ---- a3 score S = W V + gamma V, pass by pass
+            for (int pass = 0; pass < npass; ++pass) {
+                const int n0 = pass * P.NP;
+                const int ncols = min(P.NP, np - n0);
+                for (int kb = 0; kb < nkb; ++kb, ++it_count) {
+                    const uint32_t st = it_count & 1u;
+                    const uint32_t use = it_count >> 1;
+                    const uint32_t As = A0 + st * (kTM * kKB);
+                    const uint32_t Bs = B0 + st * P.b_stage;
+                    if (it_count >= 2) mbar_wait(mma_bar0 + 8 * st, (use - 1) & 1u);   // stage free
+                    if (m == 0) {
+                        mbar_expect_tx(tma_bar0 + 8 * st, (uint32_t)ncols * kKB);
+                        for (int r0 = 0; r0 < ncols; r0 += P.BR)
+                            tma_load_2d(Bs + r0 * kKB, &wmap, tma_bar0 + 8 * st, kb * kKB, n0 + r0);
+                    }
+                    // A tile: probe m's bits [kb*128, kb*128+128) as bytes, 128 B swizzle
+                    {
+                        const int w0 = kb * 4;
+                        uint32_t wv[4];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) wv[q] = (w0 + q < nw) ? V[(w0 + q) * kTM + m] : 0u;
+                        uint8_t *arow = gbase + (As - base) + m * kKB;
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch) {
+                            const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
+                            uint4 v4 = make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
+                                                  spread4((bits >> 8) & 15u), spread4(bits >> 12));
+                            *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) = v4;
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncthreads();
+                    if (m == 0) {
+                        mbar_wait(tma_bar0 + 8 * st, use & 1u);
+                        tc_fence_after();
+#pragma unroll
+                        for (int ks = 0; ks < kKB / 32; ++ks) {
+                            const uint64_t ad = sw128_desc(As + ks * 32);
+                            for (int j = 0; j * 256 < ncols; ++j) {
+                                const int n = min(256, ncols - j * 256);
+                                const uint64_t bd = sw128_desc(Bs + j * 256 * kKB + ks * 32);
+                                umma_i8(tmem + j * 256, ad, bd, i8_idesc(n), (kb > 0 || ks > 0) ? 1u : 0u);
+                            }
+                        }
+                        umma_commit(mma_bar0 + 8 * st);
+                    }
+                }
+                // wait for the pass's last commit (covers all earlier MMAs of this thread)
+                {
+                    const uint32_t last = it_count - 1;
+                    mbar_wait(mma_bar0 + 8 * (last & 1u), (last >> 1) & 1u);
+                }
+                tc_fence_after();
+                // ---- a4 per-cluster max + mask (epilogue) for this pass's clusters
+                for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
+                    const uint32_t col = (uint32_t)(c * LP - n0);
+                    if constexpr (WC <= 4) {
+                        uint32_t sc[LP];
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tmem_lane + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j] + (((vw >> j) & 1u) ? (uint32_t)gamma : 0u);
+                        }
+                        uint32_t mx = 0;
+#pragma unroll
+                        for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) word |= (sc[32 * g + j] == mx ? 1u : 0u) << j;
+                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                        }
+                    } else {
+                        uint32_t mx = 0;
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tmem_lane + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)gamma : 0u));
+                        }
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tmem_lane + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)gamma : 0u)) == mx ? 1u : 0u) << j;
+                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncthreads();   // TMEM free for the next pass; Vn complete
+            }
+            // ---- convergence (Alg. 1 "until V^{t+1} == V^t"), per probe
+            bool changed = false;
+            for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
+            if (!done) {
+                if (!changed) {
+                    done = true;
+                    status = GB_CONVERGED;
+                    iters = r;
+                } else {
+                    iters = r;
+                }
+            }
+            // V <- Vn for every probe (converged probes are fixed points, invalid rows stay 0)
+            for (int w = 0; w < nw; ++w) {
+                if (valid) V[w * kTM + m] = Vn[w * kTM + m];
+            }
+            __syncthreads();
+        }
+        // ---- a7 output
+        if (p < k) {
+            uint32_t *out = out_state + p * nw;
+            for (int w = 0; w < nw; ++w) out[w] = valid ? V[w * kTM + m] : 0u;
+            out_iters[p] = (uint16_t)(valid ? iters : 0);
+            out_status[p] = (uint8_t)(valid ? (done ? GB_CONVERGED : GB_MAX_ITERS) : GB_INVALID);
+        }
+        __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+bool plan(const Shape &s, SosParams &P, size_t &smem) {
+    if (s.Lp > 256 || s.np > 4096) return false;
+    const int per_pass = 512 / s.Lp;
+    P.NP = s.Lp * per_pass;
+    if (P.NP > s.np) P.NP = s.np;
+    int br = 256;
+    while (br > 32 && s.Lp % br) br >>= 1;
+    P.BR = br;
+    const size_t vbytes = 2ull * s.nw * kTM * 4;
+    for (;;) {
+        P.b_stage = (uint32_t)P.NP * kKB;
+        P.a_off = 0;
+        P.b_off = 2 * kTM * kKB;
+        P.v_off = P.b_off + 2 * P.b_stage;
+        P.bar_off = (uint32_t)(P.v_off + vbytes);
+        smem = P.bar_off + 64 + 1024;   // barriers, tmem slot, alignment slack
+        if (smem <= 227 * 1024) return true;
+        if (P.NP <= s.Lp) return false;
+        P.NP -= s.Lp;
+    }
+}
+
+template <int WC>
+cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                     uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    SosParams P;
+    size_t smem;
+    if (!plan(net->s, P, smem)) return cudaErrorNotSupported;
+    if (!net->wmap_ok) return cudaErrorNotSupported;
+    auto fn = sos_tc_kernel<WC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    if (smem < 120 * 1024) smem = 120 * 1024;   // one CTA per SM: it owns all 512 TMEM columns
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+    const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    fn<<<grid, kThreads, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap), P, probes, k,
+                                     gamma, max_iters, state, iters, status);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool sos_tc_supported(const Shape &s) {
+    SosParams P;
+    size_t smem;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 3 && s.Wc != 4 && s.Wc != 8) return false;
+    return plan(s, P, smem);
+}
+
+// Encode the TMA descriptor of W8 (n_p x n_p u8, row-major): box 128 B x BR
+// rows, 128-byte swizzle.  Called at gb_create (W8's address never changes).
+bool sos_tc_make_map(gb_net *net) {
+    net->wmap_ok = false;
+    SosParams P;
+    size_t smem;
+    if (!plan(net->s, P, smem)) return false;
+    void *fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fnp) {
+        cudaGetLastError();
+        return false;
+    }
+    using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    const cuuint64_t dims[2] = {(cuuint64_t)net->s.np, (cuuint64_t)net->s.np};
+    const cuuint64_t strides[1] = {(cuuint64_t)net->s.np};
+    const cuuint32_t box[2] = {(cuuint32_t)kKB, (cuuint32_t)P.BR};
+    const cuuint32_t estr[2] = {1, 1};
+    alignas(64) CUtensorMap map;
+    CUresult r = reinterpret_cast<EncodeFn>(fnp)(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8,
+                                                 2, net->w8, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    static_assert(sizeof(CUtensorMap) == sizeof(net->wmap), "CUtensorMap size");
+    memcpy(net->wmap, &map, sizeof map);
+    net->wmap_ok = (r == CUDA_SUCCESS);
+    return net->wmap_ok;
+}
+
+cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                                 uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    switch (net->s.Wc) {
+        case 1: return launch_t<1>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 2: return launch_t<2>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 3: return launch_t<3>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 4: return launch_t<4>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 8: return launch_t<8>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        default: return cudaErrorNotSupported;
+    }
+}
+
+}  // namespace gb

@@ -49,6 +49,8 @@ struct gb_net {
     cudaStream_t stage_stream[2];
     cudaEvent_t stage_event[4];
     int64_t launches;     // kernels launched by this handle (diagnostics)
+    alignas(64) unsigned char wmap[128];   // CUtensorMap of W8 for the tensor-core SOS kernel
+    bool wmap_ok;
 };
 
 namespace gb {
@@ -57,6 +59,10 @@ namespace gb {
 cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
+bool sos_tc_supported(const Shape &s);
+bool sos_tc_make_map(gb_net *net);
+cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                                 uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st);
