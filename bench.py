@@ -315,14 +315,33 @@ def main():
     value = ws * k * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel (the decode kernel, one launch per call)
-    hbm, _, peak_kind = measured_peaks()
+    hbm, bf16, peak_kind = measured_peaks()
     bytes_per_probe = 2 * c + 4 * nw + 2 + 1
-    achieved = k * bytes_per_probe / (dec_ms / 1e3) / 1e9
     kernel = net.decode_kernel(rule)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
-            "algorithmic_bytes_per_probe": bytes_per_probe, "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
-            "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
+    if kernel == "sos_tc_kernel":
+        # tensor-bound: executed int8 MACs = sum over 128-probe tiles of the tile's rounds
+        # (the tile iterates until its slowest probe stops) x 128 x n_p^2; useful = per-probe rounds.
+        it_h = out[1].cpu().numpy().view(np.uint16).astype(np.int64)
+        pad = (-k) % 128
+        tiles = np.concatenate([it_h, np.zeros(pad, np.int64)]).reshape(-1, 128).max(axis=1)
+        npad = net.n_padded
+        ops_exec = float(tiles.sum()) * 2 * 128 * npad * npad
+        ops_useful = float(it_h.sum()) * 2 * npad * npad
+        peak = 2.0 * bf16   # int8 dense = 2 x bf16 (guide's nominal 4.5 / 2.25 PFLOP/s) x measured bf16
+        achieved = ops_exec / (dec_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS(int8)",
+                "frac": achieved / peak, "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
+                "ops_per_tile_round": 2 * 128 * npad * npad, "tile_rounds": int(tiles.sum()),
+                "probe_rounds": int(it_h.sum()), "useful_frac": ops_useful / ops_exec if ops_exec else None,
+                "peak_source": peak_kind + " (2 x MEASURED_PEAKS.json bf16_tflops, int8/bf16 nominal ratio)",
+                "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
+    else:
+        achieved = k * bytes_per_probe / (dec_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
+                "algorithmic_bytes_per_probe": bytes_per_probe,
+                "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
+                "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
 
     # e2e through the C-ABI with pinned host buffers
     e2e = None

@@ -275,3 +275,15 @@ def test_determinism(gb):
         b = gpu_decode(net, pr, rule, 2, 20)
         for x, y in zip(a, b):
             np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc_kernel"), (16, 256, 0, "sos_tc_kernel"),
+                                           (4, 16, 0, "sos_tc_kernel"), (3, 3, 0, "sos_tc_kernel"),
+                                           (8, 128, 2, "decode_smem_kernel"), (8, 128, 1, "decode_smem_kernel"),
+                                           (4, 16, 2, "decode_smem_kernel"),
+                                           (16, 256, 1, "decode_generic_kernel")])
+def test_kernel_selection(gb, c, l, rule, want):
+    """The product path runs the intended sm_100a kernel for each shape/rule
+    (tensor-core SOS, shared-memory bit kernel, generic warp kernel)."""
+    net = gb.Net(c, l)
+    assert net.decode_kernel(rule) == want
