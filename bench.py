@@ -249,6 +249,7 @@ def main():
     import torch
     import gbgen
     import paper_1303_7032_b200 as gb
+    from paper_1303_7032_b200 import dist as gdist
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -261,8 +262,8 @@ def main():
     dev = torch.device("cuda", local)
 
     msgs = gbgen.messages(SEED, m, c, l)
-    probes, _ = gbgen.probes(SEED + 1, msgs, k, e, l, start=rank * k)
-    my_msgs = np.ascontiguousarray(msgs[rank::ws])
+    probes, _ = gbgen.probes(SEED + 1, msgs, k, e, l, start=gdist.weak_bounds(k, rank)[0])
+    my_msgs = np.ascontiguousarray(gdist.message_shard(msgs, rank, ws))
     msgs_d = torch.from_numpy(my_msgs.view(np.int16)).to(dev)
     probes_d = torch.from_numpy(probes.view(np.int16)).to(dev)
     net = gb.Net(c, l, device=local)
@@ -273,11 +274,7 @@ def main():
     t_dec = []
 
     def step(timed):
-        net.clear()
-        net.store(msgs_d)
-        if dist is not None:
-            dist.all_reduce(w8, op=dist.ReduceOp.MAX)
-        net.seal()
+        gdist.sharded_store(net, msgs_d)   # clear + store shard + [NCCL MAX merge] + seal
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -308,10 +305,7 @@ def main():
     launches = net.launch_count() - l0
     ms = ev0.elapsed_time(ev1)
     dec_ms = sum(a.elapsed_time(b) for a, b in t_dec) / len(t_dec)
-    tm = torch.tensor([ms, dec_ms], device=dev, dtype=torch.float64)
-    if dist is not None:
-        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-    ms, dec_ms = float(tm[0]), float(tm[1])
+    ms, dec_ms = gdist.max_over_ranks([ms, dec_ms], device=dev)
     value = ws * k * args.steps / (ms / 1e3)
 
     # roofline of the dominant kernel (the decode kernel, one launch per call)
@@ -351,11 +345,7 @@ def main():
         out_h = net.alloc_outputs(k, device=False, pin=True)
 
         def e2e_step():
-            net.clear()
-            net.store(msgs_h)
-            if dist is not None:
-                dist.all_reduce(w8, op=dist.ReduceOp.MAX)
-            net.seal()
+            gdist.sharded_store(net, msgs_h)
             net.decode(probes_h, rule, gamma=args.gamma, max_iters=args.max_iters, out=out_h)
 
         e2e_step()
@@ -369,10 +359,8 @@ def main():
             e2e_step()
         b.record(stream)
         torch.cuda.synchronize()
-        te = torch.tensor([a.elapsed_time(b)], device=dev, dtype=torch.float64)
-        if dist is not None:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": ws * k * args.e2e_steps / (float(te[0]) / 1e3), "unit": "probes/s",
+        te = gdist.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+        e2e = {"value": ws * k * args.e2e_steps / (te / 1e3), "unit": "probes/s",
                "h2d_bytes_per_step": int(my_msgs.nbytes + probes.nbytes),
                "d2h_bytes_per_step": int(k * (4 * nw + 3)),
                "how": "gb_store + gb_seal + gb_decode with pinned host buffers (library-staged, "
