@@ -71,11 +71,11 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     const uint32_t swz = ((C & (C - 1)) == 0) ? (uint32_t)(C - 1) : 0u;
     uint32_t *W = smem;
     uint32_t *X = smem + np * nw;                   // [kMaxC*WC][threads]
-    uint32_t *Z = X + kMaxC * WC * kSmemThreads;    // one all-zero bit row
+    uint32_t *Z = X + kMaxC * WC * kSmemThreads;    // one all-zero block
     const int tid = threadIdx.x;
     const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
-    const uint32_t zrow = (uint32_t)__cvta_generic_to_shared(Z);
-    if (tid < kMaxC * WC) Z[tid] = 0u;
+    const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(Z);
+    if (tid < 4) Z[tid] = 0u;
 
     // W -> shared memory with the block swizzle.
     for (int i = tid; i < np * C; i += kSmemThreads) {
@@ -184,95 +184,71 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         } else {
             // ---- a6 rounds
             while (it < T) {
-                // al[t] = next state of slot t, built in registers from the old
-                // state X (shared memory) -- synchronous rounds (R14).
-                uint32_t al[kMaxC][WC];
+                uint32_t xn[kMaxC][WC];
+                bool changed = false;
 #pragma unroll
-                for (int t = 0; t < kMaxC; ++t)
-                    if (t < (int)nslot)
+                for (int t = 0; t < kMaxC; ++t) {
+                    if (t < (int)nslot) {
+                        const int c = (slots >> (4 * t)) & 15;
+                        uint32_t alive[WC];
+                        uint32_t any = 0;
 #pragma unroll
-                        for (int u = 0; u < WC; ++u) al[t][u] = X[(t * WC + u) * kSmemThreads + tid];
-#pragma unroll
-                for (int sidx = 0; sidx < kMaxC; ++sidx) {
-                    if (sidx < (int)nslot) {
-                        // Source slot: its candidate rows are pushed into every other
-                        // target.  The first (up to) 4 rows of the lowest non-empty
-                        // word are loaded for all lanes at once (full-warp loads);
-                        // a target still not covered walks the remaining rows.
-                        const uint32_t c2 = (slots >> (4 * sidx)) & 15u;
-                        uint32_t rem[WC];
-#pragma unroll
-                        for (int u = 0; u < WC; ++u) rem[u] = X[(sidx * WC + u) * kSmemThreads + tid];
-                        uint32_t wsel = 0, usel = 0;
-#pragma unroll
-                        for (int u = WC - 1; u >= 0; --u)
-                            if (rem[u]) { wsel = rem[u]; usel = (uint32_t)u; }
-                        const uint32_t sbase = w_s + (c2 * LP + usel * 32) * rowB;
-                        uint32_t ra4[4], rk4[4];
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const bool ok = wsel != 0u;
-                            const uint32_t b = __ffs(wsel) - 1;
-                            wsel &= wsel - 1u;
-                            ra4[q] = ok ? sbase + b * rowB : zrow;
-                            rk4[q] = ok ? (b & swz) * BB : 0u;
+                        for (int u = 0; u < WC; ++u) {
+                            alive[u] = X[(t * WC + u) * kSmemThreads + tid];
+                            any |= alive[u];
                         }
+                        for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
+                            if ((int)sidx == t) continue;
+                            const int c2 = (slots >> (4 * sidx)) & 15;
+                            uint32_t h[WC];
 #pragma unroll
-                        for (int u = 0; u < WC; ++u)
-                            if ((uint32_t)u == usel) rem[u] = wsel;
+                            for (int u = 0; u < WC; ++u) h[u] = 0u;
+                            uint32_t miss = any;
+                            const uint32_t ckey = (uint32_t)c;
 #pragma unroll
-                        for (int t = 0; t < kMaxC; ++t) {
-                            if (t < (int)nslot && t != sidx) {
-                                uint32_t any = 0;
+                            for (int u2 = 0; u2 < WC; ++u2) {
+                                if (!miss) break;
+                                uint32_t cur = X[(sidx * WC + u2) * kSmemThreads + tid];
+                                // row j = c2*LP + u2*32 + b  ->  j & swz == b & swz
+                                const uint32_t base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
+                                while (cur && miss) {
+                                    // two rows per check: the second is the zero block when
+                                    // only one candidate is left (branch-free, ILP 2)
+                                    const uint32_t b1 = __ffs(cur) - 1;
+                                    cur &= cur - 1u;
+                                    const uint32_t b2 = __ffs(cur) - 1;
+                                    cur &= cur - 1u;
+                                    uint32_t r[WC], r2[WC];
+                                    lds_block<WC>(base + b1 * rowB + ((ckey ^ (b1 & swz)) * BB), r);
+                                    const uint32_t a2 = base + b2 * rowB + ((ckey ^ (b2 & swz)) * BB);
+                                    lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
+                                    miss = 0u;
 #pragma unroll
-                                for (int u = 0; u < WC; ++u) any |= al[t][u];
-                                if (any) {
-                                    const uint32_t cb = ((slots >> (4 * t)) & 15u) * BB;
-                                    uint32_t h[WC], r[WC];
-                                    lds_block<WC>(ra4[0] + (cb ^ rk4[0]), h);
-#pragma unroll
-                                    for (int q = 1; q < 4; ++q) {
-                                        lds_block<WC>(ra4[q] + (cb ^ rk4[q]), r);
-#pragma unroll
-                                        for (int u = 0; u < WC; ++u) h[u] |= r[u];
+                                    for (int u = 0; u < WC; ++u) {
+                                        h[u] |= r[u] | r2[u];
+                                        miss |= alive[u] & ~h[u];
                                     }
-                                    uint32_t miss = 0;
-#pragma unroll
-                                    for (int u = 0; u < WC; ++u) miss |= al[t][u] & ~h[u];
-                                    if (miss) {
-#pragma unroll
-                                        for (int u2 = 0; u2 < WC; ++u2) {
-                                            uint32_t cur = rem[u2];
-                                            const uint32_t base = w_s + (c2 * LP + u2 * 32) * rowB;
-                                            while (cur && miss) {
-                                                const uint32_t b = __ffs(cur) - 1;
-                                                cur &= cur - 1u;
-                                                lds_block<WC>(base + b * rowB + (cb ^ ((b & swz) * BB)), r);
-                                                miss = 0u;
-#pragma unroll
-                                                for (int u = 0; u < WC; ++u) {
-                                                    h[u] |= r[u];
-                                                    miss |= al[t][u] & ~h[u];
-                                                }
-                                            }
-                                        }
-                                    }
-#pragma unroll
-                                    for (int u = 0; u < WC; ++u) al[t][u] &= h[u];
                                 }
                             }
+                            any = 0u;
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                alive[u] &= h[u];
+                                any |= alive[u];
+                            }
                         }
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) xn[t][u] = alive[u];
                     }
                 }
-                bool changed = false;
 #pragma unroll
                 for (int t = 0; t < kMaxC; ++t) {
                     if (t < (int)nslot) {
 #pragma unroll
                         for (int u = 0; u < WC; ++u) {
                             uint32_t *a = &X[(t * WC + u) * kSmemThreads + tid];
-                            changed |= (*a != al[t][u]);
-                            *a = al[t][u];
+                            changed |= (*a != xn[t][u]);
+                            *a = xn[t][u];
                         }
                     }
                 }
@@ -306,7 +282,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
 }
 
 size_t smem_bytes(const Shape &s, int wc) {
-    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4 + kMaxC * wc * 4;
+    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4 + 16;
 }
 
 template <int WC, int RULE>
