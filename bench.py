@@ -312,7 +312,7 @@ def main():
     hbm, bf16, peak_kind = measured_peaks()
     bytes_per_probe = 2 * c + 4 * nw + 2 + 1
     kernel = net.decode_kernel(rule)
-    if kernel == "sos_tc_kernel":
+    if kernel.startswith("sos_tc"):
         # tensor-bound: executed int8 MACs = sum over 128-probe tiles of the tile's rounds
         # (the tile iterates until its slowest probe stops) x 128 x n_p^2; useful = per-probe rounds.
         it_h = out[1].cpu().numpy().view(np.uint16).astype(np.int64)

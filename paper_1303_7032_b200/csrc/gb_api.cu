@@ -150,6 +150,7 @@ int gb_destroy(gb_net *net) {
     for (int i = 0; i < 2; ++i) if (net->stage_stream[i]) cudaStreamDestroy(net->stage_stream[i]);
     for (int i = 0; i < 4; ++i) if (net->stage_event[i]) cudaEventDestroy(net->stage_event[i]);
     cudaFree(net->stage);
+    cudaFree(net->w8g);
     cudaFree(net->w8);
     cudaFree(net->wb);
     cudaFree(net->dflag);
@@ -232,6 +233,7 @@ int gb_seal(gb_net *net, void *stream) {
                     (structural & gb::kFlagPad) ? " padding edge" : "");
     }
     net->sealed = true;
+    net->seal_gen += 1;
     if (cnt) return fail(GB_EINVAL, "gb_seal: %llu stored message(s) had a symbol >= L and were skipped",
                          (unsigned long long)cnt);
     return GB_OK;
@@ -314,6 +316,7 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
+    if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s)) return "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     return "decode_generic_kernel";
@@ -335,7 +338,7 @@ cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int ru
                           cudaStream_t st) {
     cudaError_t e = cudaErrorNotSupported;
     if (rule == GB_SUM_OF_SUM) {
-        if (net->wmap_ok && sos_tc_supported(net->s))
+        if (sos_tc2_supported(net->s) || (net->wmap_ok && sos_tc_supported(net->s)))
             e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, state, iters, status, st);
     } else {
         e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);

@@ -316,6 +316,281 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
+// ---------------------------------------------------------------------------
+// v2: warp-specialised, for n_p <= 1024 (the whole expanded A tile of a round
+// fits in shared memory).  Warp 0 = TMA producer (W tiles, S-stage ring),
+// warp 1 = MMA issuer (one elected lane) and TMEM owner, warps 2-5 = the 128
+// epilogue threads (probe = TMEM lane).  TMEM holds two 256-column
+// accumulators, so the epilogue of pass p overlaps the MMAs of pass p+1.
+// gamma*V is folded into the B operand (W8 + gamma*I, built per gamma) when
+// gamma <= 255, so the epilogue is max + compare only.
+struct Sos2Params {
+    int NP;          // columns per pass (whole clusters, <= 256)
+    int BR;          // TMA box rows
+    int S;           // B stages
+    int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    uint32_t a_off, b_off, v_off, bar_off, b_stage;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
+template <int WC>
+__global__ void __launch_bounds__(192, 1)
+sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
+               const uint16_t *__restrict__ probes, int64_t k, int T,
+               uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
+               uint8_t *__restrict__ out_status) {
+    constexpr int LP = 32 * WC;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t A0 = base + P.a_off;     // nkb x (128 x 128 B), SW128
+    const uint32_t B0 = base + P.b_off;     // S x (NP x 128 B), SW128
+    uint32_t *Vs = reinterpret_cast<uint32_t *>(gbase + P.v_off);   // 2 x [nw][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
+    // bars: full[0..S) empty[S..2S) tfull[2S..2S+2) tempty[2S+2..2S+4); then tmem slot
+    const uint32_t bar0 = smem_u32(bars);
+    const int S = P.S;
+    auto full_bar = [&](int i) { return bar0 + 8u * i; };
+    auto empty_bar = [&](int i) { return bar0 + 8u * (S + i); };
+    auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * S + i); };
+    auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * S + 2 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool epi = warp >= 2;
+    const int m = 32 * (warp & 3) + lane;            // probe row = TMEM lane (epilogue warps)
+    const int nw = s.nw, np = s.np;
+    const int nkb = (np + kKB - 1) / kKB;
+    const int npass = (np + P.NP - 1) / P.NP;
+
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(tfull_bar(i), 1); mbar_init(tempty_bar(i), 128); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&wmap) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    uint32_t it_p = 0, it_m = 0, pc_m = 0, pc_e = 0;   // pipeline counters (per role)
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t p = tile * kTM + m;
+        uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+        bool done = true, valid = false;
+        int iters = 0;
+        if (epi) {
+            // ---- a1 ingest: V^0 known one-hot, erased 0
+            if (p < k) {
+                valid = true;
+                for (int c = 0; c < s.C; ++c) {
+                    const unsigned sym = __ldg(probes + p * s.C + c);
+                    if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+                }
+                done = !valid;
+            }
+            for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
+            if (valid)
+                for (int c = 0; c < s.C; ++c) {
+                    const unsigned sym = __ldg(probes + p * s.C + c);
+                    if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
+                }
+        }
+        for (int r = 1; r <= T; ++r) {
+            if (__syncthreads_and(epi ? done : true)) break;
+            if (epi) {
+                // A = V^T as bytes, one 128 x 128 B swizzled tile per K block
+                for (int kb = 0; kb < nkb; ++kb) {
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) wv[q] = (kb * 4 + q < nw) ? V[(kb * 4 + q) * kTM + m] : 0u;
+                    uint8_t *arow = gbase + P.a_off + kb * (kTM * kKB) + m * kKB;
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch) {
+                        const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
+                        *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
+                            make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
+                                       spread4((bits >> 8) & 15u), spread4(bits >> 12));
+                    }
+                }
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            }
+            __syncthreads();
+            if (warp == 0) {
+                if (lane == 0) {   // ---- TMA producer: W rows of each pass, K block by K block
+                    for (int pass = 0; pass < npass; ++pass) {
+                        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                        for (int kb = 0; kb < nkb; ++kb, ++it_p) {
+                            const int st = it_p % S;
+                            mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
+                            mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);
+                            const uint32_t Bs = B0 + st * P.b_stage;
+                            for (int r0 = 0; r0 < ncols; r0 += P.BR)
+                                tma_load_2d(Bs + r0 * kKB, &wmap, full_bar(st), kb * kKB, n0 + r0);
+                        }
+                    }
+                }
+                __syncwarp();
+            } else if (warp == 1) {
+                if (lane == 0) {   // ---- MMA issuer
+                    for (int pass = 0; pass < npass; ++pass, ++pc_m) {
+                        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                        const uint32_t buf = pc_m & 1u;
+                        mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
+                        tc_fence_after();
+                        const uint32_t idesc = i8_idesc(ncols);
+                        for (int kb = 0; kb < nkb; ++kb, ++it_m) {
+                            const int st = it_m % S;
+                            mbar_wait(full_bar(st), (it_m / S) & 1u);
+                            tc_fence_after();
+                            const uint32_t As = A0 + kb * (kTM * kKB), Bs = B0 + st * P.b_stage;
+#pragma unroll
+                            for (int ks = 0; ks < kKB / 32; ++ks)
+                                umma_i8(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32), idesc,
+                                        (kb > 0 || ks > 0) ? 1u : 0u);
+                            umma_commit(empty_bar(st));
+                        }
+                        umma_commit(tfull_bar(buf));
+                    }
+                }
+                __syncwarp();
+            } else {
+                // ---- epilogue: per-cluster max + mask of each pass (a4)
+                const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+                for (int pass = 0; pass < npass; ++pass, ++pc_e) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    const uint32_t buf = pc_e & 1u;
+                    mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
+                    tc_fence_after();
+                    for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
+                        const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
+                        if constexpr (WC <= 4) {
+                            uint32_t sc[LP];
+#pragma unroll
+                            for (int g = 0; g < WC; ++g) {
+                                uint32_t v32[32];
+                                tmem_ld32(tl + col + 32 * g, v32);
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
+                            }
+                            if (P.gamma_epi) {
+#pragma unroll
+                                for (int g = 0; g < WC; ++g) {
+                                    const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                                    for (int j = 0; j < 32; ++j)
+                                        sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
+                                }
+                            }
+                            uint32_t mx = 0;
+#pragma unroll
+                            for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
+                            const uint32_t mx1 = mx - 1u;   // sc == mx  <=>  (mx - 1 - sc) has the sign bit
+#pragma unroll
+                            for (int g = 0; g < WC; ++g) {
+                                uint32_t word = 0;
+#pragma unroll
+                                for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
+                                Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            }
+                        } else {
+                            uint32_t mx = 0;
+                            for (int g = 0; g < WC; ++g) {
+                                uint32_t v32[32];
+                                tmem_ld32(tl + col + 32 * g, v32);
+                                const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                            }
+                            for (int g = 0; g < WC; ++g) {
+                                uint32_t v32[32];
+                                tmem_ld32(tl + col + 32 * g, v32);
+                                const uint32_t vw = V[(c * WC + g) * kTM + m];
+                                uint32_t word = 0;
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
+                                Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            }
+                        }
+                    }
+                    tc_fence_before();
+                    mbar_arrive(tempty_bar(buf));
+                }
+                // ---- convergence (Alg. 1 "until V^{t+1} == V^t"), per probe
+                bool changed = false;
+                for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
+                if (!done) {
+                    iters = r;
+                    if (!changed) done = true;
+                }
+                if (valid)
+                    for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+            }
+        }
+        if (epi && p < k) {   // ---- a7 output
+            uint32_t *out = out_state + p * nw;
+            for (int w = 0; w < nw; ++w) out[w] = valid ? V[w * kTM + m] : 0u;
+            out_iters[p] = (uint16_t)(valid ? iters : 0);
+            out_status[p] = (uint8_t)(valid ? (done ? GB_CONVERGED : GB_MAX_ITERS) : GB_INVALID);
+        }
+        __syncthreads();
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+bool plan2(const Shape &s, int gamma, Sos2Params &P, size_t &smem) {
+    if (s.Lp > 256 || s.np > 1024) return false;
+    P.NP = s.Lp * (256 / s.Lp);
+    if (P.NP > s.np) P.NP = s.np;
+    int br = 256;
+    while (br > 32 && s.Lp % br) br >>= 1;
+    P.BR = br;
+    P.gamma_epi = gamma > 255 ? gamma : 0;
+    const int nkb = (s.np + kKB - 1) / kKB;
+    P.a_off = 0;
+    P.b_off = (uint32_t)nkb * kTM * kKB;
+    P.b_stage = (uint32_t)P.NP * kKB;
+    const size_t vbytes = 2ull * s.nw * kTM * 4;
+    for (P.S = 4; P.S >= 2; --P.S) {
+        P.v_off = P.b_off + P.S * P.b_stage;
+        P.bar_off = (uint32_t)(P.v_off + vbytes);
+        smem = P.bar_off + 8 * (2 * P.S + 4) + 16 + 1024;
+        if (smem <= 227 * 1024) return true;
+    }
+    return false;
+}
+
+// W8g = W8 + gamma*I on the real neurons (the B operand of sos_tc2_kernel).
+__global__ void diag_kernel(Shape s, const uint8_t *__restrict__ w8, uint8_t *__restrict__ w8g, int gamma) {
+    const int64_t n16 = (int64_t)s.np * s.np / 16;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += (int64_t)gridDim.x * blockDim.x) {
+        uint4 v = reinterpret_cast<const uint4 *>(w8)[i];
+        const int64_t b0 = i * 16;
+        const int64_t row = b0 / s.np, col0 = b0 - row * s.np;
+        if (row >= col0 && row < col0 + 16 && (row % s.Lp) < s.L) {
+            uint8_t *bytes = reinterpret_cast<uint8_t *>(&v);
+            bytes[row - col0] = (uint8_t)gamma;
+        }
+        reinterpret_cast<uint4 *>(w8g)[i] = v;
+    }
+}
+
 bool plan(const Shape &s, SosParams &P, size_t &smem) {
     if (s.Lp > 256 || s.np > 4096) return false;
     const int per_pass = 512 / s.Lp;
@@ -400,8 +675,88 @@ bool sos_tc_make_map(gb_net *net) {
     return net->wmap_ok;
 }
 
+namespace {
+
+template <int WC>
+cudaError_t launch2_t(gb_net *net, const Sos2Params &P, size_t smem, const uint16_t *probes, int64_t k,
+                      int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    auto fn = sos_tc2_kernel<WC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+    const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    fn<<<grid, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_g), P, probes, k,
+                                max_iters, state, iters, status);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
+bool encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
+    void *fnp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fnp) {
+        cudaGetLastError();
+        return false;
+    }
+    using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    const cuuint64_t dims[2] = {(cuuint64_t)net->s.np, (cuuint64_t)net->s.np};
+    const cuuint64_t strides[1] = {(cuuint64_t)net->s.np};
+    const cuuint32_t box[2] = {(cuuint32_t)kKB, (cuuint32_t)box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    alignas(64) CUtensorMap map;
+    CUresult r = reinterpret_cast<EncodeFn>(fnp)(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, gaddr, dims, strides, box,
+                                                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    memcpy(out, &map, sizeof map);
+    return r == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool sos_tc2_supported(const Shape &s) {
+    Sos2Params P;
+    size_t smem;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 3 && s.Wc != 4 && s.Wc != 8) return false;
+    return plan2(s, 1, P, smem);
+}
+
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    Sos2Params P2;
+    size_t smem2;
+    if (plan2(net->s, gamma, P2, smem2) &&
+        (net->s.Wc == 1 || net->s.Wc == 2 || net->s.Wc == 3 || net->s.Wc == 4 || net->s.Wc == 8)) {
+        // B operand W8 + gamma*I (rebuilt after each seal or gamma change)
+        if (!net->w8g) {
+            if (cudaMalloc(&net->w8g, (size_t)net->s.np * net->s.np) != cudaSuccess) {
+                cudaGetLastError();
+                net->w8g = nullptr;
+                return cudaErrorMemoryAllocation;
+            }
+            if (!encode_map(net, net->w8g, P2.BR, net->wmap_g)) return cudaErrorNotSupported;
+            net->w8g_gen = ~0ull;
+        }
+        const int gfold = gamma > 255 ? 0 : gamma;
+        if (net->w8g_gen != net->seal_gen || net->w8g_gamma != gfold) {
+            diag_kernel<<<net->sm_count * 4, 256, 0, st>>>(net->s, net->w8, net->w8g, gfold);
+            net->launches += 1;
+            cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) return e;
+            net->w8g_gen = net->seal_gen;
+            net->w8g_gamma = gfold;
+        }
+        if (smem2 < 120 * 1024) smem2 = 120 * 1024;   // one CTA per SM (512 TMEM columns)
+        switch (net->s.Wc) {
+            case 1: return launch2_t<1>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+            case 2: return launch2_t<2>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+            case 3: return launch2_t<3>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+            case 4: return launch2_t<4>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+            default: return launch2_t<8>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+        }
+    }
     switch (net->s.Wc) {
         case 1: return launch_t<1>(net, probes, k, gamma, max_iters, state, iters, status, st);
         case 2: return launch_t<2>(net, probes, k, gamma, max_iters, state, iters, status, st);

@@ -51,6 +51,10 @@ struct gb_net {
     int64_t launches;     // kernels launched by this handle (diagnostics)
     alignas(64) unsigned char wmap[128];   // CUtensorMap of W8 for the tensor-core SOS kernel
     bool wmap_ok;
+    uint8_t *w8g;                          // W8 + gamma*I (B operand of sos_tc2_kernel), lazily built
+    alignas(64) unsigned char wmap_g[128];
+    int w8g_gamma;
+    unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
 };
 
 namespace gb {
@@ -60,6 +64,7 @@ cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cud
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
 bool sos_tc_supported(const Shape &s);
+bool sos_tc2_supported(const Shape &s);
 bool sos_tc_make_map(gb_net *net);
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);

@@ -163,7 +163,8 @@ def test_config2_shape_parity(gb, m):
 
 
 @pytest.mark.parametrize("c,l,m,e", [(3, 3, 4, 2), (5, 33, 200, 2), (7, 100, 3000, 3), (2, 1, 1, 1),
-                                     (6, 64, 500, 6), (8, 128, 0, 4), (12, 40, 800, 5)])
+                                     (6, 64, 500, 6), (8, 128, 0, 4), (12, 40, 800, 5),
+                                     (4, 256, 2000, 2), (8, 256, 3000, 4)])
 def test_odd_shapes_and_degenerate(gb, c, l, m, e):
     """Ragged clusters (L not a multiple of 32, padding), L=1, M=0, e=C."""
     run_case(gb, c, l, m, 300, e, seed=c * 100 + l)
@@ -194,7 +195,7 @@ def test_invalid_probes_and_gamma_range(gb):
     pr[::5, 1] = 16
     pr[1::7, 0] = 0xFFFE
     for rule in RULES:
-        for g in (1, 3, 200):
+        for g in (1, 3, 200, 255, 256, 300):
             assert_same(gpu_decode(net, pr, rule, g, 20), oracle.decode(w, c, l, pr, rule, g, 20), rule)
     assert_same(gpu_decode(net, pr, 0, 0, 20), oracle.decode(w, c, l, pr, 0, 0, 20), 0)
     for T in (1, 2, 3):
@@ -277,8 +278,9 @@ def test_determinism(gb):
             np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc_kernel"), (16, 256, 0, "sos_tc_kernel"),
-                                           (4, 16, 0, "sos_tc_kernel"), (3, 3, 0, "sos_tc_kernel"),
+@pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc2_kernel"), (16, 256, 0, "sos_tc_kernel"),
+                                           (4, 16, 0, "sos_tc2_kernel"), (3, 3, 0, "sos_tc2_kernel"),
+                                           (8, 256, 0, "sos_tc_kernel"), (4, 256, 0, "sos_tc2_kernel"),
                                            (8, 128, 2, "decode_smem_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_generic_kernel")])
