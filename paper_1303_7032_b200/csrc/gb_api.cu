@@ -121,9 +121,10 @@ int gb_create(int c, int l, int device, gb_net **out) {
     const size_t w8b = (size_t)s.np * s.np, wbb = (size_t)s.np * s.nw * sizeof(uint32_t);
     if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb) != cudaSuccess ||
         cudaMalloc(&net->dflag, sizeof(unsigned)) != cudaSuccess ||
-        cudaMalloc(&net->dcount, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaMalloc(&net->dcount, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&net->queue, sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dflag); cudaFree(net->dcount);
+        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dflag); cudaFree(net->dcount); cudaFree(net->queue);
         free(net);
         return fail(GB_ENOMEM, "gb_create: device allocation of W (%zu bytes)", w8b + wbb);
     }
@@ -155,6 +156,7 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->wb);
     cudaFree(net->dflag);
     cudaFree(net->dcount);
+    cudaFree(net->queue);
     free(net);
     return GB_OK;
 }

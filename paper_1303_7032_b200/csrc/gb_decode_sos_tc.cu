@@ -339,7 +339,7 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 template <int WC>
 __global__ void __launch_bounds__(192, 1)
 sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
-               const uint16_t *__restrict__ probes, int64_t k, int T,
+               const uint16_t *__restrict__ probes, int64_t k, int T, unsigned long long *queue,
                uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
                uint8_t *__restrict__ out_status) {
     constexpr int LP = 32 * WC;
@@ -385,169 +385,180 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
     const uint32_t tmem = *tmem_slot;
 
     uint32_t it_p = 0, it_m = 0, pc_m = 0, pc_e = 0;   // pipeline counters (per role)
-    const int64_t ntiles = (k + kTM - 1) / kTM;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t p = tile * kTM + m;
-        uint32_t *V = Vs, *Vn = Vs + nw * kTM;
-        bool done = true, valid = false;
-        int iters = 0;
-        if (epi) {
-            // ---- a1 ingest: V^0 known one-hot, erased 0
-            if (p < k) {
-                valid = true;
-                for (int c = 0; c < s.C; ++c) {
-                    const unsigned sym = __ldg(probes + p * s.C + c);
-                    if (sym != kErased && sym >= (unsigned)s.L) valid = false;
-                }
-                done = !valid;
-            }
+    // Slot refill ("continuous batching", N4): each TMEM lane is a slot holding
+    // one probe; when its probe converges or reaches max_iters its result is
+    // written and the slot takes the next probe from a global queue, so no
+    // slot idles while a straggler in the same tile keeps iterating.  Rounds
+    // stay synchronous per probe; a probe's rounds are counted locally.
+    uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+    int64_t p = -1;
+    int rl = 0;            // rounds run by the slot's current probe
+    bool active = false;
+    auto refill = [&]() {
+        for (;;) {
+            p = (int64_t)atomicAdd(queue, 1ull);
             for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
-            if (valid)
-                for (int c = 0; c < s.C; ++c) {
-                    const unsigned sym = __ldg(probes + p * s.C + c);
-                    if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
-                }
-        }
-        for (int r = 1; r <= T; ++r) {
-            if (__syncthreads_and(epi ? done : true)) break;
-            if (epi) {
-                // A = V^T as bytes, one 128 x 128 B swizzled tile per K block
-                for (int kb = 0; kb < nkb; ++kb) {
-                    uint32_t wv[4];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) wv[q] = (kb * 4 + q < nw) ? V[(kb * 4 + q) * kTM + m] : 0u;
-                    uint8_t *arow = gbase + P.a_off + kb * (kTM * kKB) + m * kKB;
-#pragma unroll
-                    for (int ch = 0; ch < 8; ++ch) {
-                        const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
-                        *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
-                            make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
-                                       spread4((bits >> 8) & 15u), spread4(bits >> 12));
-                    }
-                }
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            rl = 0;
+            if (p >= k) { active = false; return; }
+            bool valid = true;
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased && sym >= (unsigned)s.L) valid = false;
             }
-            __syncthreads();
-            if (warp == 0) {
-                if (lane == 0) {   // ---- TMA producer: W rows of each pass, K block by K block
-                    for (int pass = 0; pass < npass; ++pass) {
-                        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
-                        for (int kb = 0; kb < nkb; ++kb, ++it_p) {
-                            const int st = it_p % S;
-                            mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
-                            mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);
-                            const uint32_t Bs = B0 + st * P.b_stage;
-                            for (int r0 = 0; r0 < ncols; r0 += P.BR)
-                                tma_load_2d(Bs + r0 * kKB, &wmap, full_bar(st), kb * kKB, n0 + r0);
-                        }
-                    }
-                }
-                __syncwarp();
-            } else if (warp == 1) {
-                if (lane == 0) {   // ---- MMA issuer
-                    for (int pass = 0; pass < npass; ++pass, ++pc_m) {
-                        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
-                        const uint32_t buf = pc_m & 1u;
-                        mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
-                        tc_fence_after();
-                        const uint32_t idesc = i8_idesc(ncols);
-                        for (int kb = 0; kb < nkb; ++kb, ++it_m) {
-                            const int st = it_m % S;
-                            mbar_wait(full_bar(st), (it_m / S) & 1u);
-                            tc_fence_after();
-                            const uint32_t As = A0 + kb * (kTM * kKB), Bs = B0 + st * P.b_stage;
-#pragma unroll
-                            for (int ks = 0; ks < kKB / 32; ++ks)
-                                umma_i8(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32), idesc,
-                                        (kb > 0 || ks > 0) ? 1u : 0u);
-                            umma_commit(empty_bar(st));
-                        }
-                        umma_commit(tfull_bar(buf));
-                    }
-                }
-                __syncwarp();
-            } else {
-                // ---- epilogue: per-cluster max + mask of each pass (a4)
-                const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-                for (int pass = 0; pass < npass; ++pass, ++pc_e) {
-                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
-                    const uint32_t buf = pc_e & 1u;
-                    mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
-                    tc_fence_after();
-                    for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
-                        const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
-                        if constexpr (WC <= 4) {
-                            uint32_t sc[LP];
-#pragma unroll
-                            for (int g = 0; g < WC; ++g) {
-                                uint32_t v32[32];
-                                tmem_ld32(tl + col + 32 * g, v32);
-#pragma unroll
-                                for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
-                            }
-                            if (P.gamma_epi) {
-#pragma unroll
-                                for (int g = 0; g < WC; ++g) {
-                                    const uint32_t vw = V[(c * WC + g) * kTM + m];
-#pragma unroll
-                                    for (int j = 0; j < 32; ++j)
-                                        sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
-                                }
-                            }
-                            uint32_t mx = 0;
-#pragma unroll
-                            for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
-                            const uint32_t mx1 = mx - 1u;   // sc == mx  <=>  (mx - 1 - sc) has the sign bit
-#pragma unroll
-                            for (int g = 0; g < WC; ++g) {
-                                uint32_t word = 0;
-#pragma unroll
-                                for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
-                                Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
-                            }
-                        } else {
-                            uint32_t mx = 0;
-                            for (int g = 0; g < WC; ++g) {
-                                uint32_t v32[32];
-                                tmem_ld32(tl + col + 32 * g, v32);
-                                const uint32_t vw = V[(c * WC + g) * kTM + m];
-#pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
-                            }
-                            for (int g = 0; g < WC; ++g) {
-                                uint32_t v32[32];
-                                tmem_ld32(tl + col + 32 * g, v32);
-                                const uint32_t vw = V[(c * WC + g) * kTM + m];
-                                uint32_t word = 0;
-#pragma unroll
-                                for (int j = 0; j < 32; ++j)
-                                    word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
-                                Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
-                            }
-                        }
-                    }
-                    tc_fence_before();
-                    mbar_arrive(tempty_bar(buf));
-                }
-                // ---- convergence (Alg. 1 "until V^{t+1} == V^t"), per probe
-                bool changed = false;
-                for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
-                if (!done) {
-                    iters = r;
-                    if (!changed) done = true;
-                }
-                if (valid)
-                    for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+            if (!valid) {   // GB_INVALID: zero state, 0 rounds; take another probe
+                uint32_t *out = out_state + p * nw;
+                for (int w = 0; w < nw; ++w) out[w] = 0u;
+                out_iters[p] = 0;
+                out_status[p] = GB_INVALID;
+                continue;
             }
+            // ---- a1 ingest: V^0 known one-hot, erased 0 (PAPER.md L197)
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
+            }
+            active = true;
+            return;
         }
-        if (epi && p < k) {   // ---- a7 output
-            uint32_t *out = out_state + p * nw;
-            for (int w = 0; w < nw; ++w) out[w] = valid ? V[w * kTM + m] : 0u;
-            out_iters[p] = (uint16_t)(valid ? iters : 0);
-            out_status[p] = (uint8_t)(valid ? (done ? GB_CONVERGED : GB_MAX_ITERS) : GB_INVALID);
+    };
+    if (epi) refill();
+    for (;;) {
+        if (!__syncthreads_or(epi && active)) break;
+        if (epi) {
+            // A = V^T as bytes, one 128 x 128 B swizzled tile per K block
+            for (int kb = 0; kb < nkb; ++kb) {
+                uint32_t wv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) wv[q] = (kb * 4 + q < nw) ? V[(kb * 4 + q) * kTM + m] : 0u;
+                uint8_t *arow = gbase + P.a_off + kb * (kTM * kKB) + m * kKB;
+#pragma unroll
+                for (int ch = 0; ch < 8; ++ch) {
+                    const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
+                    *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
+                        make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
+                                   spread4((bits >> 8) & 15u), spread4(bits >> 12));
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();
+        if (warp == 0) {
+            if (lane == 0) {   // ---- TMA producer: W rows of each pass, K block by K block
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    for (int kb = 0; kb < nkb; ++kb, ++it_p) {
+                        const int st = it_p % S;
+                        mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
+                        mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);
+                        const uint32_t Bs = B0 + st * P.b_stage;
+                        for (int r0 = 0; r0 < ncols; r0 += P.BR)
+                            tma_load_2d(Bs + r0 * kKB, &wmap, full_bar(st), kb * kKB, n0 + r0);
+                    }
+                }
+            }
+            __syncwarp();
+        } else if (warp == 1) {
+            if (lane == 0) {   // ---- MMA issuer
+                for (int pass = 0; pass < npass; ++pass, ++pc_m) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    const uint32_t buf = pc_m & 1u;
+                    mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t idesc = i8_idesc(ncols);
+                    for (int kb = 0; kb < nkb; ++kb, ++it_m) {
+                        const int st = it_m % S;
+                        mbar_wait(full_bar(st), (it_m / S) & 1u);
+                        tc_fence_after();
+                        const uint32_t As = A0 + kb * (kTM * kKB), Bs = B0 + st * P.b_stage;
+#pragma unroll
+                        for (int ks = 0; ks < kKB / 32; ++ks)
+                            umma_i8(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32), idesc,
+                                    (kb > 0 || ks > 0) ? 1u : 0u);
+                        umma_commit(empty_bar(st));
+                    }
+                    umma_commit(tfull_bar(buf));
+                }
+            }
+            __syncwarp();
+        } else {
+            // ---- epilogue: per-cluster max + mask of each pass (a4)
+            const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+            for (int pass = 0; pass < npass; ++pass, ++pc_e) {
+                const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                const uint32_t buf = pc_e & 1u;
+                mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
+                tc_fence_after();
+                for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
+                    const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
+                    if constexpr (WC <= 4) {
+                        uint32_t sc[LP];
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
+                        }
+                        if (P.gamma_epi) {
+#pragma unroll
+                            for (int g = 0; g < WC; ++g) {
+                                const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
+                            }
+                        }
+                        uint32_t mx = 0;
+#pragma unroll
+                        for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
+                        const uint32_t mx1 = mx - 1u;   // sc == mx  <=>  (mx - 1 - sc) has the sign bit
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
+                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                        }
+                    } else {
+                        uint32_t mx = 0;
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                        }
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
+                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(tempty_bar(buf));
+            }
+            // ---- convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
+            if (active) {
+                ++rl;
+                bool changed = false;
+                for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
+                for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+                if (!changed || rl == T) {   // ---- a7 output
+                    uint32_t *out = out_state + p * nw;
+                    for (int w = 0; w < nw; ++w) out[w] = V[w * kTM + m];
+                    out_iters[p] = (uint16_t)rl;
+                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    refill();
+                }
+            }
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -685,8 +696,10 @@ cudaError_t launch2_t(gb_net *net, const Sos2Params &P, size_t smem, const uint1
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
     fn<<<grid, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_g), P, probes, k,
-                                max_iters, state, iters, status);
+                                max_iters, net->queue, state, iters, status);
     net->launches += 1;
     return cudaGetLastError();
 }

@@ -55,6 +55,7 @@ struct gb_net {
     alignas(64) unsigned char wmap_g[128];
     int w8g_gamma;
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
+    unsigned long long *queue;             // device work counter (slot-refill kernels)
 };
 
 namespace gb {
