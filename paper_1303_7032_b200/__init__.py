@@ -25,7 +25,7 @@ ERASED = 0xFFFF
 GB_OK, GB_EINVAL, GB_ENOMEM, GB_ECUDA, GB_ESTATE, GB_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgb.so")
+LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB: experiment builds
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_seal",

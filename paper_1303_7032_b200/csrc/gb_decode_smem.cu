@@ -36,7 +36,7 @@
 namespace gb {
 namespace {
 
-constexpr int kSmemThreads = 768;
+constexpr int kSmemThreads = 640;
 constexpr int kMaxC = 8;
 
 template <int WC>
