@@ -39,6 +39,7 @@ CONFIGS = {
     "c2": (8, 128, 5000, 4, 2, 100_000, "BASELINE C2 point: c=8 l=128 M=5k e=4, 10^5 probes"),
     "c1": (4, 16, 50, 2, 2, 1000, "BASELINE C1: c=4 l=16 M=50 e=2, 1000 probes"),
     "c4": (16, 256, 100000, 8, 1, 1_000_000, "BASELINE C4: c=16 l=256 M=100k e=8, 10^6 probes"),
+    "c5": (16, 256, 10_000_000, 0, -1, 0, "BASELINE C5: store of 10^7 messages at c=16 l=256 (sharded, NCCL MAX merge)"),
 }
 SEED = 0x5EED
 
@@ -214,6 +215,77 @@ def config_dict(args, cfg, ws):
             "seed": SEED}
 
 
+def run_store(args, cfg):
+    """C5: storage scaling.  Step = gb_clear + gb_store(this rank's M/N messages) + NCCL MAX merge of
+    W8 (uint8) + gb_seal.  Strong scaling: M fixed, sharded over the ranks."""
+    import numpy as np
+    import torch
+    import gbgen
+    import paper_1303_7032_b200 as gb
+    from paper_1303_7032_b200 import dist as gdist
+    c, l, m, e, rule, k, desc = cfg
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    lo, hi = gdist.strong_bounds(m, rank, ws)
+    if args.impl == "reference":
+        if rank == 0:
+            import oracle
+            os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+            n = 200_000
+            msgs = gbgen.messages(SEED, n, c, l)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                oracle.store(msgs, c, l)
+            v = n * args.steps / (time.perf_counter() - t0)
+            print(json.dumps({"impl": "reference", "metric": "messages stored/sec (C5)", "value": v,
+                              "unit": "messages/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                              "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+                              "data": "synthetic", "config": {"workload": desc},
+                              "cpu_baseline": {"value": v, "unit": "messages/s", "cores": 1, "kind": "oracle",
+                                               "sample": f"{n} messages per step"},
+                              "e2e": {"value": v, "unit": "messages/s", "h2d_bytes_per_step": 0,
+                                      "d2h_bytes_per_step": 0}}), flush=True)
+        return 0
+    msgs = gbgen.messages(SEED, m, c, l) if m <= 20_000_000 else None
+    shard = torch.from_numpy(np.ascontiguousarray(msgs[lo:hi]).view(np.int16)).to(dev)
+    net = gb.Net(c, l, device=local)
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        gdist.sharded_store(net, shard)
+    torch.cuda.synchronize()
+    l0 = net.launch_count()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        gdist.sharded_store(net, shard)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = gdist.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+    value = m * args.steps / (ms / 1e3)
+    hbm, _, kind = measured_peaks()
+    np_ = net.n_padded
+    # algorithmic bytes per step: message input 2C B each + W8 (u8 n_p^2) written + seal read/packed
+    alg = (hi - lo) * 2 * c + np_ * np_ + 2 * np_ * np_ + np_ * np_ // 8
+    achieved = alg / (ms / args.steps / 1e3) / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "messages stored/sec (C5 storage scaling)", "value": value, "unit": "messages/s",
+            "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (gbgen, seed 0x5EED)",
+            "config": {"workload": desc, "c": c, "l": l, "M": m, "messages_per_gpu": hi - lo,
+                       "edge_writes_per_message": c * (c - 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "kernel": "store_kernel+seal_kernel",
+                         "note": "scattered u8 edge writes are L2-resident (W8 16 MiB); bytes = inputs + W8 + seal"},
+            "gpu_launches": net.launch_count() - l0}), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -242,6 +314,8 @@ def main():
         desc = f"c={c} l={l} M={m} e={e} {RULE_NAMES[rule]}, {k} probes/GPU"
     cfg = (c, l, m, e, rule, k, desc)
     args.warmup = max(args.warmup, 3)
+    if args.config == "c5":
+        return run_store(args, cfg)
     if args.impl == "reference":
         return run_reference(args, cfg)
 
