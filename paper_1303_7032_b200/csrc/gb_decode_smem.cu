@@ -114,6 +114,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             out_status[p] = GB_INVALID;
             continue;
         }
+        const unsigned scope = (RULE == GB_SUM_OF_MAX) ? ((1u << C) - 1u) : emask;   // in-scope clusters
         // slot list: erased clusters (hybrid) or all clusters (SOM); 4 bits each
         unsigned slots = 0, nslot = 0;
 #pragma unroll
@@ -256,24 +257,35 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 if (!changed) { status = GB_CONVERGED; break; }
             }
         }
-        // ---- a7 output (known clusters one-hot, slots from X)
-        unsigned slot_of = 0;  // 4 bits per cluster: slot index + 1 (0 = none)
-        for (unsigned t = 0; t < nslot; ++t) slot_of |= (t + 1) << (4 * ((slots >> (4 * t)) & 15));
+        // ---- a7 output: clusters outside the scope are the known one-hot; slots come from X
 #pragma unroll
         for (int c = 0; c < kMaxC; ++c) {
-            if (c >= C) break;
-            const unsigned so = (slot_of >> (4 * c)) & 15u;
-            uint32_t v[WC];
+            if (c < C && !((scope >> c) & 1u)) {
+                const unsigned sc = (unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 0xffffu;
+                uint32_t v[WC];
 #pragma unroll
-            for (int u = 0; u < WC; ++u)
-                v[u] = so ? X[((so - 1) * WC + u) * kSmemThreads + tid]
-                          : ((((unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 0xffffu) >> 5) == (unsigned)u
-                                 ? (1u << ((unsigned)(((c < 4) ? sp_lo : sp_hi) >> (16 * (c & 3))) & 31u)) : 0u);
-            if constexpr (WC == 4) {
-                *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
-            } else {
+                for (int u = 0; u < WC; ++u) v[u] = ((sc >> 5) == (unsigned)u) ? (1u << (sc & 31)) : 0u;
+                if constexpr (WC == 4) {
+                    *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
+                } else {
 #pragma unroll
-                for (int u = 0; u < WC; ++u) out[c * WC + u] = v[u];
+                    for (int u = 0; u < WC; ++u) out[c * WC + u] = v[u];
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kMaxC; ++t) {
+            if (t < (int)nslot) {
+                const unsigned c = (slots >> (4 * t)) & 15u;
+                uint32_t v[WC];
+#pragma unroll
+                for (int u = 0; u < WC; ++u) v[u] = X[(t * WC + u) * kSmemThreads + tid];
+                if constexpr (WC == 4) {
+                    *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) out[c * WC + u] = v[u];
+                }
             }
         }
         out_iters[p] = (uint16_t)it;
