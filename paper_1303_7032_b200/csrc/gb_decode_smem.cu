@@ -206,29 +206,33 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             for (int u = 0; u < WC; ++u) h[u] = 0u;
                             uint32_t miss = any;
                             const uint32_t ckey = (uint32_t)c;
+                            // one loop over the source's candidate words (a lane that runs out of
+                            // word u2 moves on inside the same loop: no per-word divergent tails)
+                            const uint32_t *xs = X + (sidx * WC) * kSmemThreads + tid;
+                            uint32_t u2 = 0, cur = xs[0];
+                            uint32_t base = w_s + (uint32_t)(c2 * LP) * rowB;   // row j = c2*LP + u2*32 + b
+                            while (miss) {
+                                if (!cur) {
+                                    do { ++u2; } while (u2 < (uint32_t)WC && !(cur = xs[u2 * kSmemThreads]));
+                                    if (u2 >= (uint32_t)WC) break;
+                                    base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
+                                }
+                                // two rows per check: the second is the zero block when only
+                                // one candidate is left in the word (branch-free, ILP 2);
+                                // j & swz == b & swz since c2*LP + u2*32 is a multiple of 8
+                                const uint32_t b1 = __ffs(cur) - 1;
+                                cur &= cur - 1u;
+                                const uint32_t b2 = __ffs(cur) - 1;
+                                cur &= cur - 1u;
+                                uint32_t r[WC], r2[WC];
+                                lds_block<WC>(base + b1 * rowB + ((ckey ^ (b1 & swz)) * BB), r);
+                                const uint32_t a2 = base + b2 * rowB + ((ckey ^ (b2 & swz)) * BB);
+                                lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
+                                miss = 0u;
 #pragma unroll
-                            for (int u2 = 0; u2 < WC; ++u2) {
-                                if (!miss) break;
-                                uint32_t cur = X[(sidx * WC + u2) * kSmemThreads + tid];
-                                // row j = c2*LP + u2*32 + b  ->  j & swz == b & swz
-                                const uint32_t base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
-                                while (cur && miss) {
-                                    // two rows per check: the second is the zero block when
-                                    // only one candidate is left (branch-free, ILP 2)
-                                    const uint32_t b1 = __ffs(cur) - 1;
-                                    cur &= cur - 1u;
-                                    const uint32_t b2 = __ffs(cur) - 1;
-                                    cur &= cur - 1u;
-                                    uint32_t r[WC], r2[WC];
-                                    lds_block<WC>(base + b1 * rowB + ((ckey ^ (b1 & swz)) * BB), r);
-                                    const uint32_t a2 = base + b2 * rowB + ((ckey ^ (b2 & swz)) * BB);
-                                    lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
-                                    miss = 0u;
-#pragma unroll
-                                    for (int u = 0; u < WC; ++u) {
-                                        h[u] |= r[u] | r2[u];
-                                        miss |= alive[u] & ~h[u];
-                                    }
+                                for (int u = 0; u < WC; ++u) {
+                                    h[u] |= r[u] | r2[u];
+                                    miss |= alive[u] & ~h[u];
                                 }
                             }
                             any = 0u;
