@@ -321,6 +321,7 @@ const char *gb_decode_kernel(gb_net *net, int rule) {
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s)) return "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
+    if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule)) return "decode_l2_kernel";
     return "decode_generic_kernel";
 }
 
@@ -344,6 +345,7 @@ cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int ru
             e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, state, iters, status, st);
     } else {
         e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
+        if (e == cudaErrorNotSupported) e = launch_decode_l2(net, probes, k, rule, max_iters, state, iters, status, st);
     }
     if (e != cudaErrorNotSupported) return e;
     return launch_decode_generic(net, probes, k, rule, gamma, max_iters, state, iters, status, st);

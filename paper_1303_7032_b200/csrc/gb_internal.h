@@ -64,6 +64,9 @@ namespace gb {
 cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
+bool decode_l2_supported(const Shape &s, int rule);
+cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 bool sos_tc_supported(const Shape &s);
 bool sos_tc2_supported(const Shape &s);
 bool sos_tc_make_map(gb_net *net);

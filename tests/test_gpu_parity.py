@@ -283,7 +283,9 @@ def test_determinism(gb):
                                            (8, 256, 0, "sos_tc_kernel"), (4, 256, 0, "sos_tc2_kernel"),
                                            (8, 128, 2, "decode_smem_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
-                                           (16, 256, 1, "decode_generic_kernel")])
+                                           (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
+                                           (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_generic_kernel"),
+                                           (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
     (tensor-core SOS, shared-memory bit kernel, generic warp kernel)."""
