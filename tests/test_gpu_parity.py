@@ -164,7 +164,8 @@ def test_config2_shape_parity(gb, m):
 
 @pytest.mark.parametrize("c,l,m,e", [(3, 3, 4, 2), (5, 33, 200, 2), (7, 100, 3000, 3), (2, 1, 1, 1),
                                      (6, 64, 500, 6), (8, 128, 0, 4), (12, 40, 800, 5),
-                                     (4, 256, 2000, 2), (8, 256, 3000, 4)])
+                                     (4, 256, 2000, 2), (8, 256, 3000, 4), (9, 70, 400, 4), (10, 64, 900, 5),
+                                     (20, 16, 300, 10)])
 def test_odd_shapes_and_degenerate(gb, c, l, m, e):
     """Ragged clusters (L not a multiple of 32, padding), L=1, M=0, e=C."""
     run_case(gb, c, l, m, 300, e, seed=c * 100 + l)
@@ -284,7 +285,8 @@ def test_determinism(gb):
                                            (8, 128, 2, "decode_smem_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
-                                           (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_generic_kernel"),
+                                           (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2_kernel"),
+                                           (9, 70, 1, "decode_generic_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
