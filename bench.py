@@ -388,9 +388,9 @@ def main():
     kernel = net.decode_kernel(rule)
     if kernel.startswith("sos_tc"):
         # tensor-bound.  Algorithmic int8 ops = sum over probes of its rounds x 2 n_p^2 (Eq.(11) per
-        # probe-round).  sos_tc_kernel (n_p > 1024) runs 128-probe tiles to the tile's slowest probe,
-        # so it executes tile-rounds x 128 x 2 n_p^2; sos_tc2_kernel refills converged slots, so its
-        # executed work is the algorithmic work plus the last partial rounds.
+        # probe-round).  Both SOS kernels refill converged slots of their 128-probe tiles, so the
+        # executed work is the algorithmic work plus the last partial rounds (a fixed-tile kernel
+        # would execute tile-rounds x 128 x 2 n_p^2, reported for comparison).
         it_h = out[1].cpu().numpy().view(np.uint16).astype(np.int64)
         pad = (-k) % 128
         tiles = np.concatenate([it_h, np.zeros(pad, np.int64)]).reshape(-1, 128).max(axis=1)
@@ -403,8 +403,8 @@ def main():
                 "frac": achieved / peak, "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
                 "ops_per_probe_round": 2 * npad * npad, "probe_rounds": int(it_h.sum()),
                 "tile_rounds_if_no_refill": int(tiles.sum()),
-                "ops_basis": "algorithmic (per-probe rounds)" if kernel == "sos_tc2_kernel" else
-                             "algorithmic; the kernel executes tile-rounds (%.3g ops)" % ops_tile,
+                "ops_basis": "algorithmic (per-probe rounds); the kernels refill converged TMEM lanes, so "
+                             "executed work = algorithmic + the partial last rounds",
                 "peak_source": peak_kind + " (2 x MEASURED_PEAKS.json bf16_tflops, int8/bf16 nominal ratio)",
                 "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
     else:

@@ -113,7 +113,7 @@ struct SosParams {
 template <int WC>
 __global__ void __launch_bounds__(kThreads, 1)
 sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
-              const uint16_t *__restrict__ probes, int64_t k, int gamma, int T,
+              const uint16_t *__restrict__ probes, int64_t k, int gamma, int T, unsigned long long *queue,
               uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
               uint8_t *__restrict__ out_status) {
     constexpr int LP = 32 * WC;
@@ -154,35 +154,44 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
     const uint32_t tmem_lane = tmem + ((uint32_t)(warp * 32) << 16);
 
     uint32_t it_count = 0;   // K-block iterations issued so far (stage/phase bookkeeping)
-    const int64_t ntiles = (k + kTM - 1) / kTM;
-
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int64_t p = tile * kTM + m;
-        uint32_t *V = Vs, *Vn = Vs + nw * kTM;
-        // ---- a1 ingest: V^0 = known one-hot, erased clusters 0
-        bool done = true;   // converged, invalid or beyond k
-        int status = GB_MAX_ITERS, iters = 0;
-        bool valid = false;
-        if (p < k) {
-            valid = true;
+    // Slot refill (as in sos_tc2_kernel): each TMEM lane holds one probe; a probe
+    // that converges or reaches max_iters is written out and replaced by the
+    // next probe of the global queue.
+    uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+    int64_t p = -1;
+    int rl = 0;
+    bool active = false;
+    auto refill = [&]() {
+        for (;;) {
+            p = (int64_t)atomicAdd(queue, 1ull);
+            for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
+            rl = 0;
+            if (p >= k) { active = false; return; }
+            bool valid = true;
             for (int c = 0; c < s.C; ++c) {
                 const unsigned sym = __ldg(probes + p * s.C + c);
                 if (sym != kErased && sym >= (unsigned)s.L) valid = false;
             }
-            done = !valid;
-            if (!valid) status = GB_INVALID;
-        }
-        for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
-        if (valid) {
+            if (!valid) {
+                uint32_t *out = out_state + p * nw;
+                for (int w = 0; w < nw; ++w) out[w] = 0u;
+                out_iters[p] = 0;
+                out_status[p] = GB_INVALID;
+                continue;
+            }
+            // ---- a1 ingest: V^0 = known one-hot, erased clusters 0
             for (int c = 0; c < s.C; ++c) {
                 const unsigned sym = __ldg(probes + p * s.C + c);
                 if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
             }
+            active = true;
+            return;
         }
-        __syncthreads();
-
-        for (int r = 1; r <= T; ++r) {
-            if (__syncthreads_and(done)) break;
+    };
+    refill();
+    {
+        for (;;) {
+            if (!__syncthreads_or(active)) break;
             // ---- a3 score S = W V + gamma V, pass by pass
             for (int pass = 0; pass < npass; ++pass) {
                 const int n0 = pass * P.NP;
@@ -284,30 +293,21 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
                 tc_fence_before();
                 __syncthreads();   // TMEM free for the next pass; Vn complete
             }
-            // ---- convergence (Alg. 1 "until V^{t+1} == V^t"), per probe
-            bool changed = false;
-            for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
-            if (!done) {
-                if (!changed) {
-                    done = true;
-                    status = GB_CONVERGED;
-                    iters = r;
-                } else {
-                    iters = r;
+            // ---- convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
+            if (active) {
+                ++rl;
+                bool changed = false;
+                for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
+                for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+                if (!changed || rl == T) {   // ---- a7 output
+                    uint32_t *out = out_state + p * nw;
+                    for (int w = 0; w < nw; ++w) out[w] = V[w * kTM + m];
+                    out_iters[p] = (uint16_t)rl;
+                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    refill();
                 }
             }
-            // V <- Vn for every probe (converged probes are fixed points, invalid rows stay 0)
-            for (int w = 0; w < nw; ++w) {
-                if (valid) V[w * kTM + m] = Vn[w * kTM + m];
-            }
             __syncthreads();
-        }
-        // ---- a7 output
-        if (p < k) {
-            uint32_t *out = out_state + p * nw;
-            for (int w = 0; w < nw; ++w) out[w] = valid ? V[w * kTM + m] : 0u;
-            out_iters[p] = (uint16_t)(valid ? iters : 0);
-            out_status[p] = (uint8_t)(valid ? (done ? GB_CONVERGED : GB_MAX_ITERS) : GB_INVALID);
         }
         __syncthreads();
     }
@@ -639,8 +639,10 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, 
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
     fn<<<grid, kThreads, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap), P, probes, k,
-                                     gamma, max_iters, state, iters, status);
+                                     gamma, max_iters, net->queue, state, iters, status);
     net->launches += 1;
     return cudaGetLastError();
 }
