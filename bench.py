@@ -40,7 +40,11 @@ CONFIGS = {
     "c1": (4, 16, 50, 2, 2, 1000, "BASELINE C1: c=4 l=16 M=50 e=2, 1000 probes"),
     "c4": (16, 256, 100000, 8, 1, 1_000_000, "BASELINE C4: c=16 l=256 M=100k e=8, 10^6 probes"),
     "c5": (16, 256, 10_000_000, 0, -1, 0, "BASELINE C5: store of 10^7 messages at c=16 l=256 (sharded, NCCL MAX merge)"),
+    # the paper's Scenario 2: its only published runtime (14.86 s for
+    # 30000 probes on a Tesla C1060 => 2019 probes/s) is quoted as vs_baseline context.
+    "s2": (16, 512, 50000, 7, 2, 30000, "Scenario 2 (PAPER.md L731): c=16 l=512 M=50k e=7 hybrid, 30000 probes"),
 }
+PAPER_BASELINE = {"s2": 30000 / 14.86}
 SEED = 0x5EED
 
 
@@ -462,7 +466,10 @@ def main():
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "probes/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+                "scaling": "weak",
+                "vs_baseline": (value / PAPER_BASELINE[args.config]) if (args.config in PAPER_BASELINE and
+                                                                        rule == CONFIGS[args.config][4]) else None,
+                "dtype": "u32",
                 "data": "synthetic (gbgen splitmix64, seed 0x5EED; iid uniform symbols, uniform erasures)",
                 "config": config_dict(args, cfg, ws), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clocks}
