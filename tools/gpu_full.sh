@@ -1,5 +1,6 @@
 #!/bin/bash
-# Full measurement pass (round artefacts): gpu tests, default bench, launch list, ncu captures.
+# Full measurement pass (round artefacts): gpu tests, default bench, reference arm, launch list,
+# ncu captures of the hybrid (C3), SOS (C2) and L2 (C4 SOM) kernels, side configs.
 TAG=$1
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests -m gpu -q 2>&1 | tail -3 > gpurun_out/tests_$TAG.txt
@@ -8,10 +9,12 @@ python bench.py > gpurun_out/bench_full_$TAG.json 2> gpurun_out/bench_full_$TAG.
 cat gpurun_out/bench_full_$TAG.json
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2>&1
 tail -1 gpurun_out/bench_ref_$TAG.json
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_smem -s 3 -c 1 -o gpurun_out/prof_hyb_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 100000 > /dev/null 2>&1
-for a in "--config c2 --rule 0" "--config c2 --rule 1" "--config c2 --rule 2" "--config c4 --rule 0 --probes 100000" "--config c4 --rule 1 --probes 100000" "--config c1 --rule 2"; do
-  timeout 300 python bench.py --no-cpu --no-e2e --steps 5 $a >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_l2 -s 3 -c 1 -o gpurun_out/prof_l2_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c4 --rule 1 --probes 100000 > /dev/null 2>&1
+rm -f gpurun_out/bench_rules_$TAG.jsonl
+for a in "--config c2 --rule 0" "--config c2 --rule 1" "--config c2 --rule 2" "--config c2 --rule 0 --probes 1000000" "--config c4 --rule 0 --probes 100000" "--config c4 --rule 1 --probes 100000" "--config c4 --rule 2" "--config c1 --rule 2" "--config s2 --rule 2" "--config c5"; do
+  timeout 300 python bench.py --no-cpu --no-e2e --steps 10 $a >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
 done
 ls gpurun_out | tail -20
