@@ -4,9 +4,10 @@
 //
 // Layout (DESIGN.md §Kernels / "smem bit kernel"):
 //  * W bit rows copied once per CTA into shared memory (128 KiB at c=8
-//    l=128).  Row j holds C blocks of WC words; block c of row j is stored
-//    at block slot (c ^ (j & m)), m = C-1 for power-of-two C (else 0), so
-//    the rows that different lanes read land in different bank groups.
+//    l=128), row-major: block c of row j = words [c*WC, c*WC+WC).  Which
+//    bank group a lane's read hits is set by its target cluster; the slot
+//    list of each probe is rotated by a lane-dependent amount so the lanes
+//    of a quarter-warp work on different targets at the same time.
 //  * one thread = one probe.  The probe's in-scope cluster states X[t][WC]
 //    (t indexes the slot list: erased clusters for the hybrid, all clusters
 //    for sum-of-max) live in a per-thread shared-memory area laid out
@@ -68,7 +69,6 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     const int nw = C * WC;
     const int np = C * LP;
     const int rowB = nw * 4;                        // bytes per row
-    const uint32_t swz = ((C & (C - 1)) == 0) ? (uint32_t)(C - 1) : 0u;
     uint32_t *W = smem;
     uint32_t *X = smem + np * nw;                   // [kMaxC*WC][threads]
     uint32_t *Z = X + kMaxC * WC * kSmemThreads;    // one all-zero block
@@ -80,7 +80,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     // W -> shared memory with the block swizzle.
     for (int i = tid; i < np * C; i += kSmemThreads) {
         const int j = i / C, c = i - j * C;
-        const int pc = c ^ (int)(j & swz);
+        const int pc = c;
 #pragma unroll
         for (int u = 0; u < WC; ++u) W[j * nw + pc * WC + u] = __ldg(wb + (int64_t)j * nw + c * WC + u);
     }
@@ -124,6 +124,15 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 ++nslot;
             }
         }
+        // rotate the slot list by a lane-dependent amount: lanes of a quarter-warp then
+        // work on different target clusters at the same static slot, which spreads
+        // their bit-row block reads over the shared-memory bank groups
+        if (nslot > 1) {
+            const unsigned rot = (unsigned)(tid & 7) % nslot;
+            const unsigned bits = 4u * nslot;
+            const unsigned msk = bits >= 32u ? 0xffffffffu : ((1u << bits) - 1u);
+            if (rot) slots = ((slots >> (4u * rot)) | (slots << (bits - 4u * rot))) & msk;
+        }
         // ---- a5 prune / init -> X.  Slots are a static unroll (their count is
         // uniform across a warp when e is); the known clusters are walked in a
         // dynamic loop of C-e trips, one bit row per known neuron.
@@ -133,8 +142,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             if (c < 4) sp_lo |= (uint64_t)(sym[c] & 0xffffu) << (16 * c);
             else sp_hi |= (uint64_t)(sym[c] & 0xffffu) << (16 * (c - 4));
         }
-        // known rows: ra[kk] = smem address of row (kc, p_kc), rk[kk] = its swizzle key * BB
-        uint32_t ra[kMaxC], rk[kMaxC];
+        // known rows: ra[kk] = smem address of row (kc, p_kc)
+        uint32_t ra[kMaxC];
         unsigned nk = 0;
         if (RULE == GB_HYBRID) {
             unsigned km = (~emask) & ((1u << C) - 1u);
@@ -145,7 +154,6 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 km &= km - 1u;
                 const unsigned sk = (unsigned)(((kc < 4) ? sp_lo : sp_hi) >> (16 * (kc & 3))) & 0xffffu;
                 ra[kk] = w_s + (kc * LP + sk) * rowB;
-                rk[kk] = (sk & swz) * BB;
             }
         }
 #pragma unroll
@@ -162,7 +170,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                         for (int kk = 0; kk < kMaxC; ++kk) {
                             if (kk < (int)nk) {
                                 uint32_t r[WC];
-                                lds_block<WC>(ra[kk] + (cb ^ rk[kk]), r);
+                                lds_block<WC>(ra[kk] + cb, r);
 #pragma unroll
                                 for (int u = 0; u < WC; ++u) x[u] &= r[u];
                             }
@@ -219,14 +227,13 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                                 }
                                 // two rows per check: the second is the zero block when only
                                 // one candidate is left in the word (branch-free, ILP 2);
-                                // j & swz == b & swz since c2*LP + u2*32 is a multiple of 8
                                 const uint32_t b1 = __ffs(cur) - 1;
                                 cur &= cur - 1u;
                                 const uint32_t b2 = __ffs(cur) - 1;
                                 cur &= cur - 1u;
                                 uint32_t r[WC], r2[WC];
-                                lds_block<WC>(base + b1 * rowB + ((ckey ^ (b1 & swz)) * BB), r);
-                                const uint32_t a2 = base + b2 * rowB + ((ckey ^ (b2 & swz)) * BB);
+                                lds_block<WC>(base + b1 * rowB + ckey * BB, r);
+                                const uint32_t a2 = base + b2 * rowB + ckey * BB;
                                 lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
                                 miss = 0u;
 #pragma unroll
