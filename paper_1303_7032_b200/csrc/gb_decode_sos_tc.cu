@@ -390,19 +390,47 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
     // written and the slot takes the next probe from a global queue, so no
     // slot idles while a straggler in the same tile keeps iterating.  Rounds
     // stay synchronous per probe; a probe's rounds are counted locally.
+    // Per-thread double buffer: the slot's current state is in buffer `par`, the
+    // epilogue writes the next state into buffer par^1 (no copy between rounds).
+    uint32_t par = 0;
     uint32_t *V = Vs, *Vn = Vs + nw * kTM;
-    int64_t p = -1;
+    int64_t p = -1, pn = -1;
+    uint4 qn = make_uint4(0, 0, 0, 0);   // prefetched symbols of probe pn (C <= 8)
+    const bool pack = s.C <= 8;
     int rl = 0;            // rounds run by the slot's current probe
     bool active = false;
+    // next probe index from the global queue; for C <= 8 its symbols are
+    // prefetched into registers so a later refill does not wait on memory
+    auto fetch = [&]() {
+        pn = (int64_t)atomicAdd(queue, 1ull);
+        if (pack && pn < k) {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+            const uint16_t *pr = probes + pn * s.C;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < s.C) w4[c >> 1] |= (uint32_t)__ldg(pr + c) << (16 * (c & 1));
+            qn = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+    };
     auto refill = [&]() {
         for (;;) {
-            p = (int64_t)atomicAdd(queue, 1ull);
-            for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
+            p = pn;
+            const uint4 q = qn;
+            fetch();
+            uint32_t *Vc = Vs + par * nw * kTM;
+            for (int w = 0; w < nw; ++w) Vc[w * kTM + m] = 0u;
             rl = 0;
             if (p >= k) { active = false; return; }
+            auto sym_of = [&](int c) -> unsigned {
+                if (pack) {
+                    const uint32_t w = (c >> 1) == 0 ? q.x : (c >> 1) == 1 ? q.y : (c >> 1) == 2 ? q.z : q.w;
+                    return (w >> (16 * (c & 1))) & 0xffffu;
+                }
+                return __ldg(probes + p * s.C + c);
+            };
             bool valid = true;
             for (int c = 0; c < s.C; ++c) {
-                const unsigned sym = __ldg(probes + p * s.C + c);
+                const unsigned sym = sym_of(c);
                 if (sym != kErased && sym >= (unsigned)s.L) valid = false;
             }
             if (!valid) {   // GB_INVALID: zero state, 0 rounds; take another probe
@@ -414,16 +442,20 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
             }
             // ---- a1 ingest: V^0 known one-hot, erased 0
             for (int c = 0; c < s.C; ++c) {
-                const unsigned sym = __ldg(probes + p * s.C + c);
-                if (sym != kErased) V[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
+                const unsigned sym = sym_of(c);
+                if (sym != kErased) Vc[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
             }
             active = true;
             return;
         }
     };
+    if (epi) fetch();
     if (epi) refill();
     for (;;) {
         if (!__syncthreads_or(epi && active)) break;
+        V = Vs + par * nw * kTM;
+        Vn = Vs + (par ^ 1u) * nw * kTM;
+        bool changed = false;
         if (epi) {
             // A = V^T as bytes, one 128 x 128 B swizzled tile per K block
             for (int kb = 0; kb < nkb; ++kb) {
@@ -517,7 +549,9 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                             uint32_t word = 0;
 #pragma unroll
                             for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
-                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            word &= real_mask(s.L, g);
+                            changed |= (word != V[(c * WC + g) * kTM + m]);
+                            Vn[(c * WC + g) * kTM + m] = word;
                         }
                     } else {
                         uint32_t mx = 0;
@@ -537,7 +571,9 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
                                 word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
-                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            word &= real_mask(s.L, g);
+                            changed |= (word != vw);
+                            Vn[(c * WC + g) * kTM + m] = word;
                         }
                     }
                 }
@@ -547,12 +583,10 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
             // ---- convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
             if (active) {
                 ++rl;
-                bool changed = false;
-                for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
-                for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+                par ^= 1u;   // V^{r} becomes the current state
                 if (!changed || rl == T) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
-                    for (int w = 0; w < nw; ++w) out[w] = V[w * kTM + m];
+                    for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
                     out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
                     refill();
