@@ -399,6 +399,10 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
     const bool pack = s.C <= 8;
     int rl = 0;            // rounds run by the slot's current probe
     bool active = false;
+    // words of A (this thread's row) that must be re-expanded before the next round;
+    // A starts undefined, so every word of every K block is dirty
+    uint32_t dirty = (nkb * 4 >= 32) ? 0xffffffffu : ((1u << (nkb * 4)) - 1u);
+    uint32_t nzcur = 0u;   // words of the current state that are non-zero
     // next probe index from the global queue; for C <= 8 its symbols are
     // prefetched into registers so a later refill does not wait on memory
     auto fetch = [&]() {
@@ -443,7 +447,11 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
             // ---- a1 ingest: V^0 known one-hot, erased 0
             for (int c = 0; c < s.C; ++c) {
                 const unsigned sym = sym_of(c);
-                if (sym != kErased) Vc[(c * WC + (sym >> 5)) * kTM + m] = 1u << (sym & 31);
+                if (sym != kErased) {
+                    const int w = c * WC + (int)(sym >> 5);
+                    Vc[w * kTM + m] = 1u << (sym & 31);
+                    dirty |= 1u << w;   // A must pick up the new probe's one-hot words
+                }
             }
             active = true;
             return;
@@ -457,20 +465,25 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
         Vn = Vs + (par ^ 1u) * nw * kTM;
         bool changed = false;
         if (epi) {
-            // A = V^T as bytes, one 128 x 128 B swizzled tile per K block
-            for (int kb = 0; kb < nkb; ++kb) {
-                uint32_t wv[4];
+            // A = V^T as bytes (128 x 128 B swizzled tile per K block), kept resident and
+            // updated incrementally: only the state words that differ from what A holds
+            // (dirty mask, n_p <= 1024 so at most 32 words) are re-expanded.
+            uint32_t d = dirty;
+            while (d) {
+                const int w = __ffs(d) - 1;
+                d &= d - 1u;
+                const uint32_t wv = (w < nw) ? V[w * kTM + m] : 0u;
+                uint8_t *arow = gbase + P.a_off + (w >> 2) * (kTM * kKB) + m * kKB;
 #pragma unroll
-                for (int q = 0; q < 4; ++q) wv[q] = (kb * 4 + q < nw) ? V[(kb * 4 + q) * kTM + m] : 0u;
-                uint8_t *arow = gbase + P.a_off + kb * (kTM * kKB) + m * kKB;
-#pragma unroll
-                for (int ch = 0; ch < 8; ++ch) {
-                    const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int ch = 2 * (w & 3) + h2;
+                    const uint32_t bits = (wv >> (h2 * 16)) & 0xffffu;
                     *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
                         make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
                                    spread4((bits >> 8) & 15u), spread4(bits >> 12));
                 }
             }
+            dirty = 0u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         __syncthreads();
@@ -550,7 +563,10 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
 #pragma unroll
                             for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
                             word &= real_mask(s.L, g);
-                            changed |= (word != V[(c * WC + g) * kTM + m]);
+                            const uint32_t old = V[(c * WC + g) * kTM + m];
+                            const uint32_t wbit = 1u << (c * WC + g);
+                            if (word != old) { changed = true; dirty |= wbit; }
+                            if (old) nzcur |= wbit;
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     } else {
@@ -572,7 +588,9 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                             for (int j = 0; j < 32; ++j)
                                 word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
                             word &= real_mask(s.L, g);
-                            changed |= (word != vw);
+                            const uint32_t wbit = 1u << (c * WC + g);
+                            if (word != vw) { changed = true; dirty |= wbit; }
+                            if (vw) nzcur |= wbit;
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     }
@@ -583,15 +601,20 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
             // ---- convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
             if (active) {
                 ++rl;
-                par ^= 1u;   // V^{r} becomes the current state
                 if (!changed || rl == T) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
                     for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
                     out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    // A still holds the expansion of the probe's state before this round
+                    // (V); the new probe's V^0 goes into the same buffer
+                    dirty |= nzcur;
                     refill();
+                } else {
+                    par ^= 1u;   // V^{r} becomes the current state
                 }
             }
+            nzcur = 0u;
         }
     }
     tc_fence_before();
