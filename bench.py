@@ -50,10 +50,27 @@ L2_FLUSH_BYTES = 512 << 20
 
 
 def dist_env():
+    """(world size, rank, local device).  GB_DIST_BACKEND=gloo (test only) lets several ranks
+    share one GPU to exercise the N>1 code path where only one GPU exists; the default is NCCL
+    with one rank per GPU."""
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("GB_DIST_BACKEND", "nccl") != "nccl":
+        import torch
+        local = local % max(1, torch.cuda.device_count())
     return ws, rank, local
+
+
+def init_dist(local):
+    import torch
+    import torch.distributed as tdist
+    backend = os.environ.get("GB_DIST_BACKEND", "nccl")
+    if backend == "nccl":
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        tdist.init_process_group(backend)
+    return tdist
 
 
 def host_cores():
@@ -232,8 +249,7 @@ def run_store(args, cfg):
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
     if ws > 1:
-        import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        tdist = init_dist(local)
     dev = torch.device("cuda", local)
     lo, hi = gdist.strong_bounds(m, rank, ws)
     if args.impl == "reference":
@@ -332,9 +348,8 @@ def main():
 
     ws, rank, local = dist_env()
     if ws > 1:
-        import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = init_dist(local)
     else:
         dist = None
         torch.cuda.set_device(local)
