@@ -163,7 +163,7 @@ class ClockSampler:
 
 def cpu_oracle_sample(msgs, probes, c, l, rule, gamma, max_iters, budget_s, gpu_out=None, idx0=0):
     """Time the CPU oracle (as it stands) on a bounded prefix of the workload."""
-    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    os.environ["OMP_NUM_THREADS"] = str(host_cores())   # all host cores (torchrun sets 1)
     import numpy as np
     import oracle
     w, _ = oracle.store(msgs, c, l)
@@ -194,7 +194,7 @@ def run_reference(args, cfg):
     per_step = max(2.0, 150.0 / max(1, args.steps + args.warmup))
     pool = min(k, 200_000)
     probes, _ = gbgen.probes(SEED + 1, msgs, pool, e, l)
-    os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+    os.environ["OMP_NUM_THREADS"] = str(host_cores())   # all host cores (torchrun sets 1)
     import oracle
     w, _ = oracle.store(msgs, c, l)
     cal = 256
@@ -255,7 +255,7 @@ def run_store(args, cfg):
     if args.impl == "reference":
         if rank == 0:
             import oracle
-            os.environ.setdefault("OMP_NUM_THREADS", str(host_cores()))
+            os.environ["OMP_NUM_THREADS"] = str(host_cores())   # all host cores (torchrun sets 1)
             n = 200_000
             msgs = gbgen.messages(SEED, n, c, l)
             t0 = time.perf_counter()
