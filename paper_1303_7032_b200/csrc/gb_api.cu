@@ -152,6 +152,7 @@ int gb_destroy(gb_net *net) {
     for (int i = 0; i < 4; ++i) if (net->stage_event[i]) cudaEventDestroy(net->stage_event[i]);
     cudaFree(net->stage);
     cudaFree(net->w8g);
+    cudaFree(net->vscratch);
     cudaFree(net->w8);
     cudaFree(net->wb);
     cudaFree(net->dflag);

@@ -106,6 +106,7 @@ __device__ __forceinline__ uint32_t real_mask(int L, int u) {
 struct SosParams {
     int NP;        // columns per pass (multiple of Lp, <= 512)
     int BR;        // TMA box rows (divides Lp, <= 256)
+    int v_global;  // state buffers in a global scratch (L2) instead of shared memory (large n_p)
     uint32_t a_off, b_off, v_off, bar_off;   // shared-memory carve (bytes from the aligned base)
     uint32_t b_stage;                        // bytes per B stage
 };
@@ -114,6 +115,7 @@ template <int WC>
 __global__ void __launch_bounds__(kThreads, 1)
 sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
               const uint16_t *__restrict__ probes, int64_t k, int gamma, int T, unsigned long long *queue,
+              uint32_t *vscratch,
               uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
               uint8_t *__restrict__ out_status) {
     constexpr int LP = 32 * WC;
@@ -123,7 +125,9 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
     uint8_t *gbase = smem_raw + (base - raw);
     const uint32_t A0 = base + P.a_off;                 // 2 stages x (128 x 128 B)
     const uint32_t B0 = base + P.b_off;                 // 2 stages x (NP x 128 B)
-    uint32_t *Vs = reinterpret_cast<uint32_t *>(gbase + P.v_off);   // [nw][128] x 2 buffers
+    // [nw][128] x 2 state buffers: shared memory, or this CTA's slice of a global scratch
+    uint32_t *Vs = P.v_global ? vscratch + (size_t)blockIdx.x * 2 * s.nw * kTM
+                              : reinterpret_cast<uint32_t *>(gbase + P.v_off);
     uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 4);
     const uint32_t tma_bar0 = smem_u32(&bars[0]), mma_bar0 = smem_u32(&bars[2]);
@@ -660,25 +664,27 @@ __global__ void diag_kernel(Shape s, const uint8_t *__restrict__ w8, uint8_t *__
 }
 
 bool plan(const Shape &s, SosParams &P, size_t &smem) {
-    if (s.Lp > 256 || s.np > 4096) return false;
-    const int per_pass = 512 / s.Lp;
-    P.NP = s.Lp * per_pass;
-    if (P.NP > s.np) P.NP = s.np;
+    if (s.Lp > 512 || s.np > 8192) return false;
     int br = 256;
     while (br > 32 && s.Lp % br) br >>= 1;
     P.BR = br;
-    const size_t vbytes = 2ull * s.nw * kTM * 4;
-    for (;;) {
-        P.b_stage = (uint32_t)P.NP * kKB;
-        P.a_off = 0;
-        P.b_off = 2 * kTM * kKB;
-        P.v_off = P.b_off + 2 * P.b_stage;
-        P.bar_off = (uint32_t)(P.v_off + vbytes);
-        smem = P.bar_off + 64 + 1024;   // barriers, tmem slot, alignment slack
-        if (smem <= 227 * 1024) return true;
-        if (P.NP <= s.Lp) return false;
-        P.NP -= s.Lp;
+    for (P.v_global = 0; P.v_global < 2; ++P.v_global) {
+        P.NP = s.Lp * (512 / s.Lp);
+        if (P.NP > s.np) P.NP = s.np;
+        const size_t vbytes = P.v_global ? 0 : 2ull * s.nw * kTM * 4;
+        for (;;) {
+            P.b_stage = (uint32_t)P.NP * kKB;
+            P.a_off = 0;
+            P.b_off = 2 * kTM * kKB;
+            P.v_off = P.b_off + 2 * P.b_stage;
+            P.bar_off = (uint32_t)(P.v_off + vbytes);
+            smem = P.bar_off + 64 + 1024;   // barriers, tmem slot, alignment slack
+            if (smem <= 227 * 1024) return true;
+            if (P.NP <= s.Lp) break;
+            P.NP -= s.Lp;
+        }
     }
+    return false;
 }
 
 template <int WC>
@@ -696,10 +702,23 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, 
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    if (P.v_global) {
+        const size_t need = (size_t)net->sm_count * 2 * net->s.nw * kTM * sizeof(uint32_t);
+        if (net->vscratch_bytes < need) {
+            cudaFree(net->vscratch);
+            net->vscratch = nullptr;
+            net->vscratch_bytes = 0;
+            if (cudaMalloc(&net->vscratch, need) != cudaSuccess) {
+                cudaGetLastError();
+                return cudaErrorMemoryAllocation;
+            }
+            net->vscratch_bytes = need;
+        }
+    }
     e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     fn<<<grid, kThreads, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap), P, probes, k,
-                                     gamma, max_iters, net->queue, state, iters, status);
+                                     gamma, max_iters, net->queue, net->vscratch, state, iters, status);
     net->launches += 1;
     return cudaGetLastError();
 }
@@ -709,7 +728,7 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, 
 bool sos_tc_supported(const Shape &s) {
     SosParams P;
     size_t smem;
-    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 3 && s.Wc != 4 && s.Wc != 8) return false;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 3 && s.Wc != 4 && s.Wc != 8 && s.Wc != 16) return false;
     return plan(s, P, smem);
 }
 
@@ -835,6 +854,7 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
         case 3: return launch_t<3>(net, probes, k, gamma, max_iters, state, iters, status, st);
         case 4: return launch_t<4>(net, probes, k, gamma, max_iters, state, iters, status, st);
         case 8: return launch_t<8>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 16: return launch_t<16>(net, probes, k, gamma, max_iters, state, iters, status, st);
         default: return cudaErrorNotSupported;
     }
 }

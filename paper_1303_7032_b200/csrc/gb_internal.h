@@ -56,6 +56,8 @@ struct gb_net {
     int w8g_gamma;
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
     unsigned long long *queue;             // device work counter (slot-refill kernels)
+    uint32_t *vscratch;                    // SOS state scratch when it does not fit shared memory
+    size_t vscratch_bytes;
 };
 
 namespace gb {

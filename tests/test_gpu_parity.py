@@ -171,6 +171,12 @@ def test_odd_shapes_and_degenerate(gb, c, l, m, e):
     run_case(gb, c, l, m, 300, e, seed=c * 100 + l)
 
 
+def test_scenario2_shape_parity(gb):
+    """The paper's Scenario 2 shape (C=16, L=512, M=50k, e=7):
+    n_padded = 8192, SOS state buffers in global scratch, W bits 8 MiB."""
+    run_case(gb, 16, 512, 50000, 24, 7, seed=2, random_count=3)
+
+
 def test_config4_shape_parity(gb):
     """BASELINE config 4 shape: c=16 l=256, M=100k, 8 erased (saturated)."""
     run_case(gb, 16, 256, 100000, 40, 8, seed=4, random_count=4)
@@ -286,7 +292,8 @@ def test_determinism(gb):
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
                                            (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2_kernel"),
-                                           (9, 70, 1, "decode_generic_kernel"),
+                                           (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc_kernel"),
+                                           (16, 512, 2, "decode_l2_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
