@@ -144,6 +144,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         }
         // known rows: ra[kk] = smem address of row (kc, p_kc)
         uint32_t ra[kMaxC];
+        // bit t*WC+u set <=> word u of slot t is non-zero (lets the push skip empty words)
+        uint32_t nzall = 0u;
         unsigned nk = 0;
         if (RULE == GB_HYBRID) {
             unsigned km = (~emask) & ((1u << C) - 1u);
@@ -182,7 +184,10 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                     for (int u = 0; u < WC; ++u) x[u] = ((sc >> 5) == (unsigned)u) ? (1u << (sc & 31)) : 0u;
                 }
 #pragma unroll
-                for (int u = 0; u < WC; ++u) X[(t * WC + u) * kSmemThreads + tid] = x[u];
+                for (int u = 0; u < WC; ++u) {
+                    X[(t * WC + u) * kSmemThreads + tid] = x[u];
+                    if (x[u]) nzall |= 1u << (t * WC + u);
+                }
             }
         }
 
@@ -217,12 +222,15 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             // one loop over the source's candidate words (a lane that runs out of
                             // word u2 moves on inside the same loop: no per-word divergent tails)
                             const uint32_t *xs = X + (sidx * WC) * kSmemThreads + tid;
-                            uint32_t u2 = 0, cur = xs[0];
-                            uint32_t base = w_s + (uint32_t)(c2 * LP) * rowB;   // row j = c2*LP + u2*32 + b
+                            uint32_t nzs = (nzall >> (sidx * WC)) & ((1u << WC) - 1u);
+                            uint32_t u2 = 0, cur = 0;
+                            uint32_t base = 0;   // row j = c2*LP + u2*32 + b
                             while (miss) {
                                 if (!cur) {
-                                    do { ++u2; } while (u2 < (uint32_t)WC && !(cur = xs[u2 * kSmemThreads]));
-                                    if (u2 >= (uint32_t)WC) break;
+                                    if (!nzs) break;   // source exhausted
+                                    u2 = __ffs(nzs) - 1;
+                                    nzs &= nzs - 1u;
+                                    cur = xs[u2 * kSmemThreads];
                                     base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
                                 }
                                 // two rows per check: the second is the zero block when only
@@ -261,6 +269,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             uint32_t *a = &X[(t * WC + u) * kSmemThreads + tid];
                             changed |= (*a != xn[t][u]);
                             *a = xn[t][u];
+                            if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
                         }
                     }
                 }
