@@ -300,3 +300,40 @@ def test_kernel_selection(gb, c, l, rule, want):
     (tensor-core SOS, shared-memory bit kernel, generic warp kernel)."""
     net = gb.Net(c, l)
     assert net.decode_kernel(rule) == want
+
+
+@pytest.mark.parametrize("rule", RULES)
+def test_config2_full_size_sampled(gb, rule):
+    """BASELINE config 2 at full size (c=8 l=128, e=4, K=10^5) for every rule and the
+    M sweep end points, in the launch configuration bench.py times: 400 sampled
+    probes checked one by one against the oracle; whole-batch properties
+    (no GB_INVALID; SOM/hybrid always converge, Thm 3 / Cor. 2)."""
+    c, l, k = 8, 128, 100_000
+    rng = np.random.default_rng(rule)
+    for m in (5000, 30000):
+        msgs = gbgen.messages(0x5EED + m, m, c, l)
+        pr, _ = gbgen.probes(0x5EED + m + 1, msgs, k, 4, l)
+        net = make_net(gb, msgs, c, l)
+        st, it, ss = gpu_decode(net, pr, rule, 2, 20)
+        assert (ss != 2).all()
+        if rule != 0:
+            assert (ss == 0).all()
+        idx = np.sort(rng.choice(k, 400, replace=False))
+        w, _ = oracle.store(msgs, c, l)
+        assert_same((st[idx], it[idx], ss[idx]), oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule,
+                    f"config2 M={m} sampled")
+
+
+def test_config4_full_size_sampled(gb):
+    """BASELINE config 4 (c=16 l=256, M=10^5, e=8) at 10^5 probes for SOS and SOM
+    (the bench's side measurement), 12 sampled probes per rule vs the oracle."""
+    c, l, m, k = 16, 256, 100_000, 100_000
+    msgs = gbgen.messages(0x5EED, m, c, l)
+    pr, _ = gbgen.probes(0x5EED + 1, msgs, k, 8, l)
+    net = make_net(gb, msgs, c, l)
+    w, _ = oracle.store(msgs, c, l)
+    idx = np.array([0, 1, 2, 777, 12345, 33333, 50000, 65432, 80000, 99997, 99998, 99999])
+    for rule in (0, 1):
+        st, it, ss = gpu_decode(net, pr, rule, 2, 20)
+        assert_same((st[idx], it[idx], ss[idx]), oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule,
+                    "config4 sampled")
