@@ -122,9 +122,10 @@ int gb_create(int c, int l, int device, gb_net **out) {
     if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb) != cudaSuccess ||
         cudaMalloc(&net->dflag, sizeof(unsigned)) != cudaSuccess ||
         cudaMalloc(&net->dcount, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&net->queue, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaMalloc(&net->queue, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&net->ovf_count, sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dflag); cudaFree(net->dcount); cudaFree(net->queue);
+        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dflag); cudaFree(net->dcount); cudaFree(net->queue); cudaFree(net->ovf_count);
         free(net);
         return fail(GB_ENOMEM, "gb_create: device allocation of W (%zu bytes)", w8b + wbb);
     }
@@ -158,6 +159,8 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->dflag);
     cudaFree(net->dcount);
     cudaFree(net->queue);
+    cudaFree(net->ovf);
+    cudaFree(net->ovf_count);
     free(net);
     return GB_OK;
 }

@@ -37,8 +37,10 @@
 namespace gb {
 namespace {
 
-constexpr int kSmemThreads = 640;
 constexpr int kMaxC = 8;
+#ifndef GB_NARROW_THREADS
+#define GB_NARROW_THREADS 768
+#endif
 
 template <int WC>
 __device__ __forceinline__ void lds_block(uint32_t addr, uint32_t (&v)[WC]) {
@@ -57,11 +59,16 @@ __device__ __forceinline__ uint32_t real_mask_u(int L, int u) {
     return nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
 }
 
-template <int WC, int RULE>
-__global__ void __launch_bounds__(kSmemThreads, 1)
+// MAXS = slots held per thread (4: hybrid probes with e <= 4 -- more threads fit;
+// 8: any probe).  A probe needing more slots than MAXS is appended to `ovf` and
+// decoded by the MAXS = 8 instance in list mode (`list` != nullptr).
+template <int WC, int RULE, int MAXS, int NT>
+__global__ void __launch_bounds__(NT, 1)
 decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes,
                    int64_t k, int T, uint32_t *__restrict__ out_state,
-                   uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status) {
+                   uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status,
+                   const int64_t *__restrict__ list, const unsigned long long *__restrict__ list_count,
+                   int64_t *__restrict__ ovf, unsigned long long *__restrict__ ovf_count) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int LP = 32 * WC;
     constexpr int BB = 4 * WC;                      // bytes per block
@@ -70,15 +77,15 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     const int np = C * LP;
     const int rowB = nw * 4;                        // bytes per row
     uint32_t *W = smem;
-    uint32_t *X = smem + np * nw;                   // [kMaxC*WC][threads]
-    uint32_t *Z = X + kMaxC * WC * kSmemThreads;    // one all-zero block
+    uint32_t *X = smem + np * nw;                   // [MAXS*WC][threads]
+    uint32_t *Z = X + MAXS * WC * NT;               // one all-zero block
     const int tid = threadIdx.x;
     const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
     const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(Z);
     if (tid < 4) Z[tid] = 0u;
 
     // W -> shared memory with the block swizzle.
-    for (int i = tid; i < np * C; i += kSmemThreads) {
+    for (int i = tid; i < np * C; i += NT) {
         const int j = i / C, c = i - j * C;
         const int pc = c;
 #pragma unroll
@@ -86,8 +93,9 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     }
     __syncthreads();
 
-    for (int64_t p = (int64_t)blockIdx.x * kSmemThreads + tid; p < k;
-         p += (int64_t)gridDim.x * kSmemThreads) {
+    const int64_t nprobe = list ? (int64_t)*list_count : k;
+    for (int64_t pi = (int64_t)blockIdx.x * NT + tid; pi < nprobe; pi += (int64_t)gridDim.x * NT) {
+        const int64_t p = list ? list[pi] : pi;
         // ---- a1 ingest
         unsigned sym[kMaxC];
         const uint16_t *pr = probes + p * C;
@@ -133,6 +141,10 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             const unsigned msk = bits >= 32u ? 0xffffffffu : ((1u << bits) - 1u);
             if (rot) slots = ((slots >> (4u * rot)) | (slots << (bits - 4u * rot))) & msk;
         }
+        if (MAXS < kMaxC && (int)nslot > MAXS) {   // needs the wide-slot instance
+            ovf[atomicAdd(ovf_count, 1ull)] = p;
+            continue;
+        }
         // ---- a5 prune / init -> X.  Slots are a static unroll (their count is
         // uniform across a warp when e is); the known clusters are walked in a
         // dynamic loop of C-e trips, one bit row per known neuron.
@@ -159,7 +171,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             }
         }
 #pragma unroll
-        for (int t = 0; t < kMaxC; ++t) {
+        for (int t = 0; t < MAXS; ++t) {
             if (t < (int)nslot) {
                 const unsigned c = (slots >> (4 * t)) & 15u;
                 uint32_t x[WC];
@@ -185,7 +197,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 }
 #pragma unroll
                 for (int u = 0; u < WC; ++u) {
-                    X[(t * WC + u) * kSmemThreads + tid] = x[u];
+                    X[(t * WC + u) * NT + tid] = x[u];
                     if (x[u]) nzall |= 1u << (t * WC + u);
                 }
             }
@@ -198,17 +210,17 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         } else {
             // ---- a6 rounds
             while (it < T) {
-                uint32_t xn[kMaxC][WC];
+                uint32_t xn[MAXS][WC];
                 bool changed = false;
 #pragma unroll
-                for (int t = 0; t < kMaxC; ++t) {
+                for (int t = 0; t < MAXS; ++t) {
                     if (t < (int)nslot) {
                         const int c = (slots >> (4 * t)) & 15;
                         uint32_t alive[WC];
                         uint32_t any = 0;
 #pragma unroll
                         for (int u = 0; u < WC; ++u) {
-                            alive[u] = X[(t * WC + u) * kSmemThreads + tid];
+                            alive[u] = X[(t * WC + u) * NT + tid];
                             any |= alive[u];
                         }
                         for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
@@ -221,7 +233,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             const uint32_t ckey = (uint32_t)c;
                             // one loop over the source's candidate words (a lane that runs out of
                             // word u2 moves on inside the same loop: no per-word divergent tails)
-                            const uint32_t *xs = X + (sidx * WC) * kSmemThreads + tid;
+                            const uint32_t *xs = X + (sidx * WC) * NT + tid;
                             uint32_t nzs = (nzall >> (sidx * WC)) & ((1u << WC) - 1u);
                             uint32_t u2 = 0, cur = 0;
                             uint32_t base = 0;   // row j = c2*LP + u2*32 + b
@@ -230,7 +242,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                                     if (!nzs) break;   // source exhausted
                                     u2 = __ffs(nzs) - 1;
                                     nzs &= nzs - 1u;
-                                    cur = xs[u2 * kSmemThreads];
+                                    cur = xs[u2 * NT];
                                     base = w_s + (uint32_t)(c2 * LP + u2 * 32) * rowB;
                                 }
                                 // two rows per check: the second is the zero block when only
@@ -262,11 +274,11 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                     }
                 }
 #pragma unroll
-                for (int t = 0; t < kMaxC; ++t) {
+                for (int t = 0; t < MAXS; ++t) {
                     if (t < (int)nslot) {
 #pragma unroll
                         for (int u = 0; u < WC; ++u) {
-                            uint32_t *a = &X[(t * WC + u) * kSmemThreads + tid];
+                            uint32_t *a = &X[(t * WC + u) * NT + tid];
                             changed |= (*a != xn[t][u]);
                             *a = xn[t][u];
                             if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
@@ -294,12 +306,12 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             }
         }
 #pragma unroll
-        for (int t = 0; t < kMaxC; ++t) {
+        for (int t = 0; t < MAXS; ++t) {
             if (t < (int)nslot) {
                 const unsigned c = (slots >> (4 * t)) & 15u;
                 uint32_t v[WC];
 #pragma unroll
-                for (int u = 0; u < WC; ++u) v[u] = X[(t * WC + u) * kSmemThreads + tid];
+                for (int u = 0; u < WC; ++u) v[u] = X[(t * WC + u) * NT + tid];
                 if constexpr (WC == 4) {
                     *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
                 } else {
@@ -313,23 +325,55 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     }
 }
 
-size_t smem_bytes(const Shape &s, int wc) {
-    return (size_t)s.np * s.nw * 4 + (size_t)kMaxC * wc * kSmemThreads * 4 + 16;
+constexpr int kWideThreads = 640;     // MAXS = 8
+constexpr int kNarrowThreads = GB_NARROW_THREADS;   // MAXS = 4
+
+size_t smem_bytes(const Shape &s, int wc, int maxs, int nt) {
+    return (size_t)s.np * s.nw * 4 + (size_t)maxs * wc * nt * 4 + 16;
+}
+
+template <int WC, int RULE, int MAXS, int NT>
+cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                     uint16_t *iters, uint8_t *status, const int64_t *list, const unsigned long long *list_count,
+                     int64_t *ovf, unsigned long long *ovf_count, cudaStream_t st) {
+    const Shape &s = net->s;
+    const size_t smem = smem_bytes(s, WC, MAXS, NT);
+    auto fn = decode_smem_kernel<WC, RULE, MAXS, NT>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = list ? net->sm_count : (k + NT - 1) / NT;
+    if (grid > net->sm_count) grid = net->sm_count;
+    fn<<<(unsigned)grid, NT, smem, st>>>(s, net->wb, probes, k, max_iters, state, iters, status, list, list_count,
+                                         ovf, ovf_count);
+    net->launches += 1;
+    return cudaGetLastError();
 }
 
 template <int WC, int RULE>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                     uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    const Shape &s = net->s;
-    const size_t smem = smem_bytes(s, WC);
-    auto fn = decode_smem_kernel<WC, RULE>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+cudaError_t launch_rule(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                        uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    if (RULE == GB_SUM_OF_MAX || net->s.C <= 4)   // every probe may need all C slots
+        return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, nullptr,
+                                                   nullptr, nullptr, nullptr, st);
+    // hybrid: probes with e <= 4 on the narrow (more threads) instance, the rest queued
+    // for the wide one (list mode)
+    if (net->ovf_cap < k) {
+        cudaFree(net->ovf);
+        net->ovf = nullptr;
+        net->ovf_cap = 0;
+        if (cudaMalloc(&net->ovf, (size_t)k * sizeof(int64_t)) != cudaSuccess) {
+            cudaGetLastError();
+            return cudaErrorMemoryAllocation;
+        }
+        net->ovf_cap = k;
+    }
+    cudaError_t e = cudaMemsetAsync(net->ovf_count, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    int64_t grid = (k + kSmemThreads - 1) / kSmemThreads;
-    if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, kSmemThreads, smem, st>>>(s, net->wb, probes, k, max_iters, state, iters, status);
-    net->launches += 1;
-    return cudaGetLastError();
+    e = launch_t<WC, RULE, 4, kNarrowThreads>(net, probes, k, max_iters, state, iters, status, nullptr, nullptr,
+                                              net->ovf, net->ovf_count, st);
+    if (e != cudaSuccess) return e;
+    return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, net->ovf,
+                                               net->ovf_count, nullptr, nullptr, st);
 }
 
 }  // namespace
@@ -337,7 +381,8 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
 bool decode_smem_supported(const Shape &s, int rule) {
     if (s.C > kMaxC || s.np > 1024 || rule == GB_SUM_OF_SUM) return false;
     if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4) return false;
-    return smem_bytes(s, s.Wc) <= 227 * 1024;
+    return smem_bytes(s, s.Wc, 8, kWideThreads) <= 227 * 1024 &&
+           smem_bytes(s, s.Wc, 4, kNarrowThreads) <= 227 * 1024;
 }
 
 // Returns cudaErrorNotSupported when the shape does not fit this kernel.
@@ -347,12 +392,12 @@ cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, i
     if (!decode_smem_supported(s, rule)) return cudaErrorNotSupported;
     const bool hyb = (rule == GB_HYBRID);
     switch (s.Wc) {
-        case 1: return hyb ? launch_t<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                           : launch_t<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 2: return hyb ? launch_t<2, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                           : launch_t<2, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        default: return hyb ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                            : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
+        case 1: return hyb ? launch_rule<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
+                           : launch_rule<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
+        case 2: return hyb ? launch_rule<2, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
+                           : launch_rule<2, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
+        default: return hyb ? launch_rule<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
+                            : launch_rule<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
     }
 }
 

@@ -57,6 +57,9 @@ struct gb_net {
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
     unsigned long long *queue;             // device work counter (slot-refill kernels)
     uint32_t *vscratch;                    // SOS state scratch when it does not fit shared memory
+    int64_t *ovf;                          // hybrid probes queued for the wide-slot smem kernel
+    int64_t ovf_cap;
+    unsigned long long *ovf_count;
     size_t vscratch_bytes;
 };
 
