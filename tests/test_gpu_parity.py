@@ -337,3 +337,17 @@ def test_config4_full_size_sampled(gb):
         st, it, ss = gpu_decode(net, pr, rule, 2, 20)
         assert_same((st[idx], it[idx], ss[idx]), oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule,
                     "config4 sampled")
+
+
+def test_mixed_erasures_narrow_and_wide_slots(gb):
+    """Hybrid probes with e <= 4 run on the 4-slot instance, the rest are queued to the
+    8-slot instance (list mode) inside the same gb_decode; per-probe e from 0 to C in
+    one batch must match the oracle for every probe (and SOM, which is all-wide)."""
+    c, l, m, k = 8, 128, 10000, 3000
+    msgs = gbgen.messages(31, m, c, l)
+    e = np.random.default_rng(5).integers(0, c + 1, size=k)
+    pr, _ = gbgen.probes(32, msgs, k, e, l, random_count=300)
+    w, _ = oracle.store(msgs, c, l)
+    net = make_net(gb, msgs, c, l)
+    for rule in (1, 2):
+        assert_same(gpu_decode(net, pr, rule, 2, 20), oracle.decode(w, c, l, pr, rule, 2, 20), rule, "mixed e")
