@@ -1,0 +1,90 @@
+"""N1: the paper's retrieval-rate experiments on the GPU path (§VII).
+
+Scenario 1 (C=8, L=128, M=5000, K=3000 stored probes, T=20):
+  * rate vs erased clusters e for SOS / SOM / hybrid (Fig. 6 / Fig. 8a-b),
+  * SOS rate vs gamma (Fig. 7),
+  mean over 5 seeds, unique exact recovery (reading R16).
+Scenario 2 (C=16, L=512, M=50000, K=30000): rate and decode time vs e
+for all three rules (Fig. 8c-d).
+
+Writes a JSON report (argv[1], default gpurun_out/sweep.json) and prints a table.
+"""
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import gbgen  # noqa: E402
+import paper_1303_7032_b200 as gb  # noqa: E402
+
+
+def onehot_words(msgs, c, l):
+    wc = (l + 31) // 32
+    out = np.zeros((msgs.shape[0], c * wc), np.uint32)
+    for cc in range(c):
+        sym = msgs[:, cc].astype(np.int64)
+        np.bitwise_or.at(out, (np.arange(msgs.shape[0]), cc * wc + (sym >> 5)),
+                         (np.uint32(1) << (sym & 31).astype(np.uint32)))
+    return out
+
+
+def run(c, l, m, k, e, rule, gamma, seed, T=20):
+    msgs = gbgen.messages(seed, m, c, l)
+    pr, src = gbgen.probes(seed + 1, msgs, k, e, l)
+    net = gb.Net(c, l)
+    net.store(torch.from_numpy(msgs.view(np.int16)).cuda())
+    net.seal()
+    pt = torch.from_numpy(pr.view(np.int16)).cuda()
+    net.decode(pt, rule, gamma=gamma, max_iters=T)   # warm-up
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    st, it, ss = net.decode(pt, rule, gamma=gamma, max_iters=T)
+    b.record()
+    torch.cuda.synchronize()
+    want = onehot_words(msgs[src], c, l)
+    ok = (st.cpu().numpy().view(np.uint32) == want).all(axis=1)
+    net.close()
+    return float(ok.mean()), float(it.cpu().numpy().view(np.uint16).mean()), a.elapsed_time(b)
+
+
+def main():
+    out = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "sweep.json")
+    rep = {"scenario1_rate_vs_e": [], "scenario1_sos_rate_vs_gamma": [], "scenario2_vs_e": []}
+    seeds = [1, 2, 3, 4, 5]
+    names = {0: "SOS", 1: "SOM", 2: "hybrid"}
+    for e in range(1, 8):
+        for rule in (0, 1, 2):
+            r = [run(8, 128, 5000, 3000, e, rule, 2, 100 * s + e) for s in seeds]
+            rep["scenario1_rate_vs_e"].append({"e": e, "rule": names[rule], "rate": float(np.mean([x[0] for x in r])),
+                                               "mean_iters": float(np.mean([x[1] for x in r]))})
+    for g in (0, 1, 2, 3, 4, 6):
+        for e in (3, 4, 5, 6):
+            r = [run(8, 128, 5000, 3000, e, 0, g, 100 * s + e) for s in seeds]
+            rep["scenario1_sos_rate_vs_gamma"].append({"gamma": g, "e": e, "rate": float(np.mean([x[0] for x in r]))})
+    for e in (1, 3, 5, 7, 9, 11, 13, 14, 15):
+        for rule in (0, 1, 2):
+            rate, iters, ms = run(16, 512, 50000, 30000, e, rule, 2, 7 + e)
+            rep["scenario2_vs_e"].append({"e": e, "rule": names[rule], "rate": rate, "mean_iters": iters,
+                                          "decode_ms": ms})
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    json.dump(rep, open(out, "w"), indent=1)
+    print("Scenario 1 (C=8 L=128 M=5000 K=3000 gamma=2 T=20), rate vs e, mean of 5 seeds")
+    for row in rep["scenario1_rate_vs_e"]:
+        print("  e=%d %-6s rate=%.3f iters=%.2f" % (row["e"], row["rule"], row["rate"], row["mean_iters"]))
+    print("Scenario 1 SOS rate vs gamma")
+    for row in rep["scenario1_sos_rate_vs_gamma"]:
+        print("  gamma=%d e=%d rate=%.3f" % (row["gamma"], row["e"], row["rate"]))
+    print("Scenario 2 (C=16 L=512 M=50000 K=30000)")
+    for row in rep["scenario2_vs_e"]:
+        print("  e=%2d %-6s rate=%.4f iters=%.2f decode=%.3f ms" % (row["e"], row["rule"], row["rate"],
+                                                                   row["mean_iters"], row["decode_ms"]))
+
+
+if __name__ == "__main__":
+    main()
