@@ -78,7 +78,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     const int rowB = nw * 4;                        // bytes per row
     uint32_t *W = smem;
     uint32_t *X = smem + np * nw;                   // [MAXS*WC][threads]
-    uint32_t *Z = X + MAXS * WC * NT;               // one all-zero block
+    uint32_t *Z = X + (MAXS == 4 ? 0 : MAXS * WC * NT);   // one all-zero block
     const int tid = threadIdx.x;
     const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
     const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(Z);
@@ -158,6 +158,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         uint32_t ra[kMaxC];
         // bit t*WC+u set <=> word u of slot t is non-zero (lets the push skip empty words)
         uint32_t nzall = 0u;
+        // 4-slot instance: the slot states live in registers (static slot indices)
+        uint32_t xr[MAXS == 4 ? 4 : 1][WC];
         unsigned nk = 0;
         if (RULE == GB_HYBRID) {
             unsigned km = (~emask) & ((1u << C) - 1u);
@@ -197,7 +199,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 }
 #pragma unroll
                 for (int u = 0; u < WC; ++u) {
-                    X[(t * WC + u) * NT + tid] = x[u];
+                    if constexpr (MAXS == 4) xr[t][u] = x[u];
+                    else X[(t * WC + u) * NT + tid] = x[u];
                     if (x[u]) nzall |= 1u << (t * WC + u);
                 }
             }
@@ -209,6 +212,84 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
             status = GB_CONVERGED;
         } else {
             // ---- a6 rounds
+            if constexpr (MAXS == 4) {
+                while (it < T) {
+                    uint32_t xn[4][WC];
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (t < (int)nslot) {
+                            const uint32_t ckey = (slots >> (4 * t)) & 15u;
+                            uint32_t alive[WC];
+                            uint32_t any = 0;
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                alive[u] = xr[t][u];
+                                any |= alive[u];
+                            }
+#pragma unroll
+                            for (int sidx = 0; sidx < 4; ++sidx) {
+                                if (sidx < (int)nslot && sidx != t && any) {
+                                    const uint32_t c2 = (slots >> (4 * sidx)) & 15u;
+                                    uint32_t h[WC];
+#pragma unroll
+                                    for (int u = 0; u < WC; ++u) h[u] = 0u;
+                                    uint32_t miss = any;
+                                    uint32_t nzs = (nzall >> (sidx * WC)) & ((1u << WC) - 1u);
+                                    uint32_t u2 = 0, cur = 0, base = 0;
+                                    while (miss) {
+                                        if (!cur) {
+                                            if (!nzs) break;   // source exhausted
+                                            u2 = __ffs(nzs) - 1;
+                                            nzs &= nzs - 1u;
+                                            cur = xr[sidx][0];
+#pragma unroll
+                                            for (int u = 1; u < WC; ++u)
+                                                if (u2 == (uint32_t)u) cur = xr[sidx][u];
+                                            base = w_s + (c2 * LP + u2 * 32) * rowB;
+                                        }
+                                        const uint32_t b1 = __ffs(cur) - 1;
+                                        cur &= cur - 1u;
+                                        const uint32_t b2 = __ffs(cur) - 1;
+                                        cur &= cur - 1u;
+                                        uint32_t r[WC], r2[WC];
+                                        lds_block<WC>(base + b1 * rowB + ckey * BB, r);
+                                        const uint32_t a2 = base + b2 * rowB + ckey * BB;
+                                        lds_block<WC>(b2 == 0xffffffffu ? zaddr : a2, r2);
+                                        miss = 0u;
+#pragma unroll
+                                        for (int u = 0; u < WC; ++u) {
+                                            h[u] |= r[u] | r2[u];
+                                            miss |= alive[u] & ~h[u];
+                                        }
+                                    }
+                                    any = 0u;
+#pragma unroll
+                                    for (int u = 0; u < WC; ++u) {
+                                        alive[u] &= h[u];
+                                        any |= alive[u];
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) xn[t][u] = alive[u];
+                        }
+                    }
+                    bool changed = false;
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (t < (int)nslot) {
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                changed |= (xr[t][u] != xn[t][u]);
+                                xr[t][u] = xn[t][u];
+                                if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
+                            }
+                        }
+                    }
+                    ++it;
+                    if (!changed) { status = GB_CONVERGED; break; }
+                }
+            } else
             while (it < T) {
                 uint32_t xn[MAXS][WC];
                 bool changed = false;
@@ -311,7 +392,10 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                 const unsigned c = (slots >> (4 * t)) & 15u;
                 uint32_t v[WC];
 #pragma unroll
-                for (int u = 0; u < WC; ++u) v[u] = X[(t * WC + u) * NT + tid];
+                for (int u = 0; u < WC; ++u) {
+                    if constexpr (MAXS == 4) v[u] = xr[t][u];
+                    else v[u] = X[(t * WC + u) * NT + tid];
+                }
                 if constexpr (WC == 4) {
                     *reinterpret_cast<uint4 *>(out + c * WC) = make_uint4(v[0], v[1], v[2], v[3]);
                 } else {
@@ -329,7 +413,8 @@ constexpr int kWideThreads = 640;     // MAXS = 8
 constexpr int kNarrowThreads = GB_NARROW_THREADS;   // MAXS = 4
 
 size_t smem_bytes(const Shape &s, int wc, int maxs, int nt) {
-    return (size_t)s.np * s.nw * 4 + (size_t)maxs * wc * nt * 4 + 16;
+    // the 4-slot instance keeps its slot states in registers (no X area)
+    return (size_t)s.np * s.nw * 4 + (maxs == 4 ? 0 : (size_t)maxs * wc * nt * 4) + 16;
 }
 
 template <int WC, int RULE, int MAXS, int NT>
