@@ -322,7 +322,8 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
-    if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s)) return "sos_tc2_kernel";
+    if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
+        return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule)) return "decode_l2_kernel";

@@ -1,0 +1,470 @@
+// gb_decode_sos_2cta.cu -- sum-of-sum decode on a CTA pair (tcgen05 cta_group::2).
+//
+// Same method and same per-probe semantics as sos_tc2_kernel (gb_decode_sos_tc.cu):
+// a3 S^t = W V^t + gamma V^t as an exact int8 x int8 -> int32 contraction
+// (Eq.(3), Eq.(10)-(11) L328/L349, Alg. 1 line 4), a4 per-cluster
+// winner-take-all with ties kept (Eq.(4)-(5) L220-225, readings R3/R4) and
+// per-probe convergence / max_iters (Alg. 1), slot refill.
+//
+// What changes is the tile: the two CTAs of a cluster (one TPC) issue one
+// UMMA of M = 256 probes (128 per CTA = its TMEM lanes), and each CTA stages
+// only HALF of the W rows of a pass (N/2 rows of the B operand); the tensor
+// core reads the other half from the peer's shared memory.  Per 256 probes a
+// round therefore moves n_p^2 bytes of W from L2 instead of 2 n_p^2, and the
+// MMA issue count halves.
+//
+//   leader (rank 0):  warp 0 TMA (its half of B, arms the pair's full barrier),
+//                     warp 1 lane 0 MMA issuer for the pair, warps 2-5 epilogue
+//   peer   (rank 1):  warp 0 TMA (its half, completes on the leader's barrier),
+//                     warps 2-5 epilogue
+// Barriers: full[S] (leader's only: expect_tx both halves), empty[S] and
+// tfull[2] in both CTAs (multicast tcgen05.commit), tempty[2] (leader's,
+// 256 arrivals: 128 local + 128 remote).  Round boundaries are cluster
+// barriers; the pair keeps iterating while either CTA has an active slot.
+#include <cuda.h>
+
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "gb_internal.h"
+#include "gb_tc_common.cuh"
+
+namespace gb {
+namespace {
+using namespace tc;
+
+struct Pair2Params {
+    int NP;          // columns per pass (whole clusters, <= 256)
+    int BR;          // TMA box rows (divides NP/2 for every pass)
+    int S;           // B stages
+    int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    uint32_t a_off, b_off, v_off, bar_off, b_stage;
+};
+
+__device__ __forceinline__ uint32_t cta_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_u32(uint32_t a, uint32_t v) {
+    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+}
+// TMA into this CTA's shared memory, transaction bytes counted on the leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t bar_leader, int x,
+                                                 int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"((uint64_t)map), "r"(bar_leader), "r"(x), "r"(y) : "memory");
+}
+// Instruction descriptor: kind::i8, D = s32, A = B = u8, K-major, M = 256 (pair), N.
+__device__ __forceinline__ uint32_t i8_idesc_pair(int n) {
+    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+// Arrive on the barrier at the same offset in both CTAs once the pair's MMAs complete.
+__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            bar),
+        "h"((uint16_t)3) : "memory");
+}
+
+template <int WC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params P,
+                 const uint16_t *__restrict__ probes, int64_t k, int T, unsigned long long *queue,
+                 uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
+                 uint8_t *__restrict__ out_status) {
+    constexpr int LP = 32 * WC;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;   // same offset in both CTAs
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t A0 = base + P.a_off;     // nkb x (128 x 128 B), SW128: this CTA's 128 probe rows
+    const uint32_t B0 = base + P.b_off;     // S x (NP/2 x 128 B), SW128: this CTA's half of the W rows
+    uint32_t *Vs = reinterpret_cast<uint32_t *>(gbase + P.v_off);   // 2 x [nw][128]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
+    const uint32_t bar0 = smem_u32(bars);
+    const int S = P.S;
+    auto full_bar = [&](int i) { return bar0 + 8u * i; };
+    auto empty_bar = [&](int i) { return bar0 + 8u * (S + i); };
+    auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * S + i); };
+    auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * S + 2 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 4);
+    uint32_t *flags = tmem_slot + 1;   // [2 round parities][2 ranks]: "has an active slot"
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool epi = warp >= 2;
+    const int m = 32 * (warp & 3) + lane;
+    const uint32_t rank = cta_rank();
+    const bool leader = rank == 0;
+    const int nw = s.nw, np = s.np;
+    const int nkb = (np + kKB - 1) / kKB;
+    const int npass = (np + P.NP - 1) / P.NP;
+
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(tfull_bar(i), 1); mbar_init(tempty_bar(i), 2 * 128); }
+        flags[0] = flags[1] = flags[2] = flags[3] = 0u;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&wmap) : "memory");
+    }
+    if (warp == 1) {   // same warp in both CTAs
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t full_leader0 = mapa(full_bar(0), 0);
+    const uint32_t tempty_leader0 = mapa(tempty_bar(0), 0);
+    const uint32_t flags_self = mapa(smem_u32(flags), rank), flags_peer = mapa(smem_u32(flags), rank ^ 1u);
+
+    uint32_t it_p = 0, it_m = 0, pc_m = 0, pc_e = 0;
+    uint32_t par = 0, round = 0;
+    uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+    int64_t p = -1, pn = -1;
+    uint4 qn = make_uint4(0, 0, 0, 0);
+    const bool pack = s.C <= 8;
+    int rl = 0;
+    bool active = false;
+    uint32_t dirty = (nkb * 4 >= 32) ? 0xffffffffu : ((1u << (nkb * 4)) - 1u);
+    uint32_t nzcur = 0u;
+    auto fetch = [&]() {
+        pn = (int64_t)atomicAdd(queue, 1ull);
+        if (pack && pn < k) {
+            uint32_t w4[4] = {0u, 0u, 0u, 0u};
+            const uint16_t *pr = probes + pn * s.C;
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+                if (c < s.C) w4[c >> 1] |= (uint32_t)__ldg(pr + c) << (16 * (c & 1));
+            qn = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
+    };
+    auto refill = [&]() {
+        for (;;) {
+            p = pn;
+            const uint4 q = qn;
+            fetch();
+            uint32_t *Vc = Vs + par * nw * kTM;
+            for (int w = 0; w < nw; ++w) Vc[w * kTM + m] = 0u;
+            rl = 0;
+            if (p >= k) { active = false; return; }
+            auto sym_of = [&](int c) -> unsigned {
+                if (pack) {
+                    const uint32_t w = (c >> 1) == 0 ? q.x : (c >> 1) == 1 ? q.y : (c >> 1) == 2 ? q.z : q.w;
+                    return (w >> (16 * (c & 1))) & 0xffffu;
+                }
+                return __ldg(probes + p * s.C + c);
+            };
+            bool valid = true;
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = sym_of(c);
+                if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+            }
+            if (!valid) {   // GB_INVALID: zero state, 0 rounds; take another probe
+                uint32_t *out = out_state + p * nw;
+                for (int w = 0; w < nw; ++w) out[w] = 0u;
+                out_iters[p] = 0;
+                out_status[p] = GB_INVALID;
+                continue;
+            }
+            for (int c = 0; c < s.C; ++c) {   // a1 ingest: V^0 known one-hot
+                const unsigned sym = sym_of(c);
+                if (sym != kErased) {
+                    const int w = c * WC + (int)(sym >> 5);
+                    Vc[w * kTM + m] = 1u << (sym & 31);
+                    dirty |= 1u << w;
+                }
+            }
+            active = true;
+            return;
+        }
+    };
+    if (epi) fetch();
+    if (epi) refill();
+    for (;;) {
+        const int loc = __syncthreads_or(epi && active);
+        if (tid == 0) {
+            const uint32_t off = 4u * (2u * (round & 1u) + rank);
+            st_cluster_u32(flags_self + off, (uint32_t)loc);
+            st_cluster_u32(flags_peer + off, (uint32_t)loc);
+        }
+        V = Vs + par * nw * kTM;
+        Vn = Vs + (par ^ 1u) * nw * kTM;
+        bool changed = false;
+        if (epi) {   // incremental A = V^T (bytes, SW128), as in sos_tc2_kernel
+            uint32_t d = dirty;
+            while (d) {
+                const int w = __ffs(d) - 1;
+                d &= d - 1u;
+                const uint32_t wv = (w < nw) ? V[w * kTM + m] : 0u;
+                uint8_t *arow = gbase + P.a_off + (w >> 2) * (kTM * kKB) + m * kKB;
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                    const int ch = 2 * (w & 3) + h2;
+                    const uint32_t bits = (wv >> (h2 * 16)) & 0xffffu;
+                    *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
+                        make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
+                                   spread4((bits >> 8) & 15u), spread4(bits >> 12));
+                }
+            }
+            dirty = 0u;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        cluster_sync();   // both A tiles ready; both flags visible
+        const uint32_t any = flags[2 * (round & 1u)] | flags[2 * (round & 1u) + 1];
+        ++round;
+        if (!any) break;
+        if (warp == 0) {
+            if (lane == 0) {   // ---- TMA producer: this CTA's half of each pass's W rows
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0), half = ncols >> 1;
+                    for (int kb = 0; kb < nkb; ++kb, ++it_p) {
+                        const int st = it_p % S;
+                        mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
+                        if (leader) mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);   // both halves
+                        const uint32_t Bs = B0 + st * P.b_stage;
+                        for (int r0 = 0; r0 < half; r0 += P.BR)
+                            tma_load_2d_pair(Bs + r0 * kKB, &wmap, full_leader0 + 8u * st, kb * kKB,
+                                             n0 + (int)rank * half + r0);
+                    }
+                }
+            }
+            __syncwarp();
+        } else if (warp == 1) {
+            if (lane == 0 && leader) {   // ---- MMA issuer for the pair
+                for (int pass = 0; pass < npass; ++pass, ++pc_m) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    const uint32_t buf = pc_m & 1u;
+                    mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t idesc = i8_idesc_pair(ncols);
+                    for (int kb = 0; kb < nkb; ++kb, ++it_m) {
+                        const int st = it_m % S;
+                        mbar_wait(full_bar(st), (it_m / S) & 1u);
+                        tc_fence_after();
+                        const uint32_t As = A0 + kb * (kTM * kKB), Bs = B0 + st * P.b_stage;
+#pragma unroll
+                        for (int ks = 0; ks < kKB / 32; ++ks)
+                            umma_i8_pair(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32),
+                                         idesc, (kb > 0 || ks > 0) ? 1u : 0u);
+                        umma_commit_pair(empty_bar(st));
+                    }
+                    umma_commit_pair(tfull_bar(buf));
+                }
+            }
+            __syncwarp();
+        } else {
+            // ---- epilogue: per-cluster max + mask of each pass (a4)
+            const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+            for (int pass = 0; pass < npass; ++pass, ++pc_e) {
+                const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                const uint32_t buf = pc_e & 1u;
+                mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
+                tc_fence_after();
+                for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
+                    const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
+                    if constexpr (WC <= 4) {
+                        uint32_t sc[LP];
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
+                        }
+                        if (P.gamma_epi) {
+#pragma unroll
+                            for (int g = 0; g < WC; ++g) {
+                                const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                                for (int j = 0; j < 32; ++j)
+                                    sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
+                            }
+                        }
+                        uint32_t mx = 0;
+#pragma unroll
+                        for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
+                        const uint32_t mx1 = mx - 1u;
+#pragma unroll
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
+                            word &= real_mask(s.L, g);
+                            const uint32_t old = V[(c * WC + g) * kTM + m];
+                            const uint32_t wbit = 1u << (c * WC + g);
+                            if (word != old) { changed = true; dirty |= wbit; }
+                            if (old) nzcur |= wbit;
+                            Vn[(c * WC + g) * kTM + m] = word;
+                        }
+                    } else {
+                        uint32_t mx = 0;
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                        }
+                        for (int g = 0; g < WC; ++g) {
+                            uint32_t v32[32];
+                            tmem_ld32(tl + col + 32 * g, v32);
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u)
+                                        << j;
+                            word &= real_mask(s.L, g);
+                            const uint32_t wbit = 1u << (c * WC + g);
+                            if (word != vw) { changed = true; dirty |= wbit; }
+                            if (vw) nzcur |= wbit;
+                            Vn[(c * WC + g) * kTM + m] = word;
+                        }
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive_cluster(tempty_leader0 + 8u * buf);
+            }
+            if (active) {   // convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
+                ++rl;
+                if (!changed || rl == T) {   // ---- a7 output
+                    uint32_t *out = out_state + p * nw;
+                    for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
+                    out_iters[p] = (uint16_t)rl;
+                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    dirty |= nzcur;
+                    refill();
+                } else {
+                    par ^= 1u;
+                }
+            }
+            nzcur = 0u;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+bool plan_pair(const Shape &s, int gamma_epi, Pair2Params &P, size_t &smem) {
+    if (s.Lp > 256 || s.np > 1024) return false;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 3 && s.Wc != 4 && s.Wc != 8) return false;
+    P.NP = s.Lp * (256 / s.Lp);
+    if (P.NP > s.np) P.NP = s.np;
+    // every pass is a multiple of Lp columns, so halves are multiples of Lp/2
+    int br = 128;
+    while (br > 8 && (s.Lp / 2) % br) br >>= 1;
+    P.BR = br;
+    P.gamma_epi = gamma_epi;
+    const int nkb = (s.np + kKB - 1) / kKB;
+    P.a_off = 0;
+    P.b_off = (uint32_t)nkb * kTM * kKB;
+    P.b_stage = (uint32_t)(P.NP / 2) * kKB;
+    P.b_stage = (P.b_stage + 1023u) & ~1023u;   // SW128 atoms stay 1024-byte aligned
+    const size_t vbytes = 2ull * s.nw * kTM * 4;
+    for (P.S = 6; P.S >= 2; --P.S) {
+        P.v_off = P.b_off + P.S * P.b_stage;
+        P.bar_off = (uint32_t)(P.v_off + vbytes);
+        smem = P.bar_off + 8 * (2 * P.S + 4) + 32 + 1024;
+        if (smem <= 227 * 1024) return true;
+    }
+    return false;
+}
+
+template <int WC>
+cudaError_t launch_pair_t(gb_net *net, const Pair2Params &P, size_t smem, const uint16_t *probes, int64_t k,
+                          int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    auto fn = sos_tc2x2_kernel<WC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // pairs that can be resident at once (TPC pairing can leave SMs unpaired)
+    static int max_clusters[9] = {0};
+    if (max_clusters[WC] == 0) {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3(2 * (unsigned)(net->sm_count / 2), 1, 1);
+        cfg.blockDim = dim3(192, 1, 1);
+        cfg.dynamicSmemBytes = smem;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = net->sm_count / 2;
+        }
+        max_clusters[WC] = n;
+    }
+    const int64_t npairs = (k + 2 * kTM - 1) / (2 * kTM);
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC]));
+    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    fn<<<2 * pairs, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_g2), P, probes, k,
+                                     max_iters, net->queue, state, iters, status);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool sos_2cta_enabled(const Shape &s) {
+    const char *env = getenv("GB_SOS_2CTA");
+    if (env && env[0] == '0') return false;
+    Pair2Params P;
+    size_t smem;
+    return plan_pair(s, 0, P, smem);
+}
+
+int sos_2cta_box_rows(const Shape &s) {
+    Pair2Params P;
+    size_t smem;
+    return plan_pair(s, 0, P, smem) ? P.BR : 0;
+}
+
+cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, int64_t k, int max_iters,
+                            uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    Pair2Params P;
+    size_t smem;
+    if (!plan_pair(net->s, gamma_epi, P, smem)) return cudaErrorNotSupported;
+    // one CTA per SM: two 512-column TMEM allocations on one SM could deadlock across pairs
+    if (smem < 120 * 1024) smem = 120 * 1024;
+    switch (net->s.Wc) {
+        case 1: return launch_pair_t<1>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        case 2: return launch_pair_t<2>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        case 3: return launch_pair_t<3>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        case 4: return launch_pair_t<4>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        default: return launch_pair_t<8>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+    }
+}
+
+}  // namespace gb

@@ -28,80 +28,13 @@
 #include <algorithm>
 
 #include "gb_internal.h"
+#include "gb_tc_common.cuh"
 
 namespace gb {
 namespace {
+using namespace tc;
 
-constexpr int kTM = 128;       // probes per tile = UMMA M
-constexpr int kKB = 128;       // K bytes per block = one 128 B swizzle atom
 constexpr int kThreads = 128;  // one thread per probe / TMEM lane
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, uint32_t bar, int x, int y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
-        ::"r"(dst), "l"((uint64_t)map), "r"(bar), "r"(x), "r"(y) : "memory");
-}
-// UMMA shared-memory descriptor, K-major, 128-byte swizzle: 8-row groups 1024 B apart.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
-    return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
-           ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
-}
-// Instruction descriptor: kind::i8, D = s32, A = B = u8, both K-major, M = 128, N.
-__device__ __forceinline__ uint32_t i8_idesc(int n) {
-    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(kTM >> 4) << 24);
-}
-__device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                        uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-__device__ __forceinline__ void umma_commit(uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-                 : "memory");
-}
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-          "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-          "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-          "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
-
-// 4 state bits -> 4 bytes of 0/1 (bit i -> byte i).
-__device__ __forceinline__ uint32_t spread4(uint32_t nib) { return (nib * 0x00204081u) & 0x01010101u; }
-
-__device__ __forceinline__ uint32_t real_mask(int L, int u) {
-    const int nb = min(32, max(0, L - u * 32));
-    return nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
-}
 
 struct SosParams {
     int NP;        // columns per pass (multiple of Lp, <= 512)
@@ -336,9 +269,6 @@ struct Sos2Params {
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
 
 template <int WC>
 __global__ void __launch_bounds__(192, 1)
@@ -782,7 +712,9 @@ cudaError_t launch2_t(gb_net *net, const Sos2Params &P, size_t smem, const uint1
     return cudaGetLastError();
 }
 
-bool encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
+}  // namespace
+
+bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
     void *fnp = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
@@ -805,8 +737,6 @@ bool encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
     return r == CUDA_SUCCESS;
 }
 
-}  // namespace
-
 bool sos_tc2_supported(const Shape &s) {
     Sos2Params P;
     size_t smem;
@@ -827,7 +757,7 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
                 net->w8g = nullptr;
                 return cudaErrorMemoryAllocation;
             }
-            if (!encode_map(net, net->w8g, P2.BR, net->wmap_g)) return cudaErrorNotSupported;
+            if (!sos_encode_map(net, net->w8g, P2.BR, net->wmap_g)) return cudaErrorNotSupported;
             net->w8g_gen = ~0ull;
         }
         const int gfold = gamma > 255 ? 0 : gamma;
@@ -838,6 +768,13 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
             if (e != cudaSuccess) return e;
             net->w8g_gen = net->seal_gen;
             net->w8g_gamma = gfold;
+        }
+        if (sos_2cta_enabled(net->s)) {
+            if (!net->wmap_g2_ok) {
+                net->wmap_g2_ok = sos_encode_map(net, net->w8g, sos_2cta_box_rows(net->s), net->wmap_g2);
+                if (!net->wmap_g2_ok) return cudaErrorNotSupported;
+            }
+            return launch_sos_2cta(net, gamma > 255 ? gamma : 0, probes, k, max_iters, state, iters, status, st);
         }
         if (smem2 < 120 * 1024) smem2 = 120 * 1024;   // one CTA per SM (512 TMEM columns)
         switch (net->s.Wc) {

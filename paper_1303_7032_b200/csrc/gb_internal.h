@@ -53,6 +53,8 @@ struct gb_net {
     bool wmap_ok;
     uint8_t *w8g;                          // W8 + gamma*I (B operand of sos_tc2_kernel), lazily built
     alignas(64) unsigned char wmap_g[128];
+    alignas(64) unsigned char wmap_g2[128];  // W8g map with the CTA-pair kernel's box (half the rows)
+    bool wmap_g2_ok;
     int w8g_gamma;
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
     unsigned long long *queue;             // device work counter (slot-refill kernels)
@@ -75,6 +77,13 @@ cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int
 bool sos_tc_supported(const Shape &s);
 bool sos_tc2_supported(const Shape &s);
 bool sos_tc_make_map(gb_net *net);
+bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out);
+// CTA-pair (cta_group::2) sum-of-sum kernel, gb_decode_sos_2cta.cu; the caller
+// has built W8g = W8 + gamma*I (gamma_epi = gamma when gamma > 255, else 0).
+bool sos_2cta_enabled(const Shape &s);
+int sos_2cta_box_rows(const Shape &s);
+cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, int64_t k, int max_iters,
+                            uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,

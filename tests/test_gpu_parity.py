@@ -4,6 +4,8 @@ Decoded states, iteration counts and statuses are integer/bit results, so the
 bar is exact equality.  Inputs come from gbgen (seeded,
 shaped like the paper's workloads).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -297,7 +299,10 @@ def test_determinism(gb):
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
-    (tensor-core SOS, shared-memory bit kernel, generic warp kernel)."""
+    (tensor-core SOS, shared-memory bit kernel, generic warp kernel).  SOS at
+    n_padded <= 1024 runs on a CTA pair (sos_tc2x2_kernel) unless GB_SOS_2CTA=0."""
+    if want == "sos_tc2_kernel" and os.environ.get("GB_SOS_2CTA", "1") != "0":
+        want = "sos_tc2x2_kernel"
     net = gb.Net(c, l)
     assert net.decode_kernel(rule) == want
 
@@ -351,3 +356,24 @@ def test_mixed_erasures_narrow_and_wide_slots(gb):
     net = make_net(gb, msgs, c, l)
     for rule in (1, 2):
         assert_same(gpu_decode(net, pr, rule, 2, 20), oracle.decode(w, c, l, pr, rule, 2, 20), rule, "mixed e")
+
+
+@pytest.mark.parametrize("c,l,m,e,gamma", [(8, 128, 8000, 4, 2), (4, 16, 60, 2, 1), (3, 3, 5, 1, 0),
+                                           (5, 33, 300, 2, 300), (4, 256, 3000, 2, 2), (6, 64, 2000, 3, 255),
+                                           (7, 100, 1500, 3, 1), (8, 96, 3000, 5, 4), (2, 1, 1, 1, 1)])
+def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
+    """The CTA-pair SOS kernel (tcgen05 cta_group::2, M = 256, each CTA stages half
+    of W's rows) and the single-CTA kernel give identical results, and both equal
+    the oracle: the pair only re-tiles the exact int32 contraction of Eq.(10)-(11)."""
+    msgs = gbgen.messages(500 + c + l, m, c, l)
+    net = make_net(gb, msgs, c, l)
+    pr, _ = gbgen.probes(501 + c, msgs, 1537, e, l, random_count=5)
+    res = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("GB_SOS_2CTA", flag)
+        res[flag] = gpu_decode(net, pr, 0, gamma, 20)
+        assert net.decode_kernel(0) == ("sos_tc2x2_kernel" if flag == "1" else "sos_tc2_kernel")
+    for x, y in zip(res["1"], res["0"]):
+        np.testing.assert_array_equal(x, y)
+    w8, _ = oracle.store(msgs, c, l)
+    assert_same(res["1"], oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20), 0, "pair")
