@@ -58,8 +58,12 @@ __device__ __forceinline__ void cluster_sync() {
 __device__ __forceinline__ void st_cluster_u32(uint32_t a, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
+// Arrive on a barrier of either CTA of the pair (address from mapa).  Default
+// .release.cta semantics: the epilogue only has to order its (waited)
+// tcgen05.ld's before the arrive, which tcgen05.fence::before_thread_sync does;
+// .release.cluster would add a GPU-scope fence behind the output stores.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 // TMA into this CTA's shared memory, transaction bytes counted on the leader's barrier.
 __device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t bar_leader, int x,
@@ -122,6 +126,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     const int nw = s.nw, np = s.np;
     const int nkb = (np + kKB - 1) / kKB;
     const int npass = (np + P.NP - 1) / P.NP;
+    const bool narrow = P.gamma_epi + np < 0x7FFF;   // scores fit 15 bits (wta_words)
 
     if (tid == 0) {
         for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
@@ -204,6 +209,20 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             return;
         }
     };
+    // producer: K block j of a round = (pass j / nkb, K block j % nkb)
+    const int nload = npass * nkb;
+    int pre = 0;   // K blocks of the coming round already issued
+    auto load_block = [&](int j) {
+        const int pass = j / nkb, kb = j - pass * nkb;
+        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0), half = ncols >> 1;
+        const int st = it_p % S;
+        mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
+        if (leader) mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);   // both halves
+        const uint32_t Bs = B0 + st * P.b_stage;
+        for (int r0 = 0; r0 < half; r0 += P.BR)
+            tma_load_2d_pair(Bs + r0 * kKB, &wmap, full_leader0 + 8u * st, kb * kKB, n0 + (int)rank * half + r0);
+        ++it_p;
+    };
     if (epi) fetch();
     if (epi) refill();
     for (;;) {
@@ -241,18 +260,12 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         if (!any) break;
         if (warp == 0) {
             if (lane == 0) {   // ---- TMA producer: this CTA's half of each pass's W rows
-                for (int pass = 0; pass < npass; ++pass) {
-                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0), half = ncols >> 1;
-                    for (int kb = 0; kb < nkb; ++kb, ++it_p) {
-                        const int st = it_p % S;
-                        mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
-                        if (leader) mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);   // both halves
-                        const uint32_t Bs = B0 + st * P.b_stage;
-                        for (int r0 = 0; r0 < half; r0 += P.BR)
-                            tma_load_2d_pair(Bs + r0 * kKB, &wmap, full_leader0 + 8u * st, kb * kKB,
-                                             n0 + (int)rank * half + r0);
-                    }
-                }
+                // W does not depend on the state, so the first `pre` K blocks of the
+                // next round are loaded at the end of this one (they land while the
+                // epilogue, the A update and the round barrier run)
+                for (int j = pre; j < nload; ++j) load_block(j);
+                pre = min(S, nload);
+                for (int j = 0; j < pre; ++j) load_block(j);
             }
             __syncwarp();
         } else if (warp == 1) {
@@ -290,12 +303,15 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                     const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
                     if constexpr (WC <= 4) {
                         uint32_t sc[LP];
+                        {   // all WC loads in flight, one wait
+                            uint32_t(&v)[LP] = sc;
 #pragma unroll
-                        for (int g = 0; g < WC; ++g) {
-                            uint32_t v32[32];
-                            tmem_ld32(tl + col + 32 * g, v32);
+                            for (int g = 0; g < WC; ++g)
+                                tmem_ld32_nw(tl + col + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * g]));
+                            tmem_wait_ld();
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
+                            for (int g = 0; g < WC; ++g)
+                                tmem_regs_ready(*reinterpret_cast<uint32_t(*)[32]>(&v[32 * g]));
                         }
                         if (P.gamma_epi) {
 #pragma unroll
@@ -306,16 +322,11 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                                     sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
                             }
                         }
-                        uint32_t mx = 0;
-#pragma unroll
-                        for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
-                        const uint32_t mx1 = mx - 1u;
+                        uint32_t wds[WC];
+                        wta_words<WC>(sc, narrow, wds);
 #pragma unroll
                         for (int g = 0; g < WC; ++g) {
-                            uint32_t word = 0;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
-                            word &= real_mask(s.L, g);
+                            const uint32_t word = wds[g] & real_mask(s.L, g);
                             const uint32_t old = V[(c * WC + g) * kTM + m];
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != old) { changed = true; dirty |= wbit; }
@@ -368,6 +379,10 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             nzcur = 0u;
         }
     }
+    // drain the prefetched loads (both halves complete on the leader's full barriers)
+    // before either CTA can exit
+    if (warp == 0 && lane == 0 && leader)
+        for (uint32_t j = it_p - (uint32_t)pre; j < it_p; ++j) mbar_wait(full_bar(j % S), (j / S) & 1u);
     tc_fence_before();
     cluster_sync();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));

@@ -301,6 +301,7 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
     const int nw = s.nw, np = s.np;
     const int nkb = (np + kKB - 1) / kKB;
     const int npass = (np + P.NP - 1) / P.NP;
+    const bool narrow = P.gamma_epi + np < 0x7FFF;   // scores fit 15 bits (wta_words)
 
     if (tid == 0) {
         for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
@@ -471,12 +472,15 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                     const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
                     if constexpr (WC <= 4) {
                         uint32_t sc[LP];
+                        {   // all WC loads in flight, one wait
+                            uint32_t(&v)[LP] = sc;
 #pragma unroll
-                        for (int g = 0; g < WC; ++g) {
-                            uint32_t v32[32];
-                            tmem_ld32(tl + col + 32 * g, v32);
+                            for (int g = 0; g < WC; ++g)
+                                tmem_ld32_nw(tl + col + 32 * g, *reinterpret_cast<uint32_t(*)[32]>(&v[32 * g]));
+                            tmem_wait_ld();
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) sc[32 * g + j] = v32[j];
+                            for (int g = 0; g < WC; ++g)
+                                tmem_regs_ready(*reinterpret_cast<uint32_t(*)[32]>(&v[32 * g]));
                         }
                         if (P.gamma_epi) {
 #pragma unroll
@@ -487,16 +491,11 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                                     sc[32 * g + j] += ((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u;
                             }
                         }
-                        uint32_t mx = 0;
-#pragma unroll
-                        for (int j = 0; j < LP; ++j) mx = max(mx, sc[j]);
-                        const uint32_t mx1 = mx - 1u;   // sc == mx  <=>  (mx - 1 - sc) has the sign bit
+                        uint32_t wds[WC];
+                        wta_words<WC>(sc, narrow, wds);
 #pragma unroll
                         for (int g = 0; g < WC; ++g) {
-                            uint32_t word = 0;
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) word |= ((mx1 - sc[32 * g + j]) >> 31) << j;
-                            word &= real_mask(s.L, g);
+                            const uint32_t word = wds[g] & real_mask(s.L, g);
                             const uint32_t old = V[(c * WC + g) * kTM + m];
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != old) { changed = true; dirty |= wbit; }

@@ -360,11 +360,15 @@ def test_mixed_erasures_narrow_and_wide_slots(gb):
 
 @pytest.mark.parametrize("c,l,m,e,gamma", [(8, 128, 8000, 4, 2), (4, 16, 60, 2, 1), (3, 3, 5, 1, 0),
                                            (5, 33, 300, 2, 300), (4, 256, 3000, 2, 2), (6, 64, 2000, 3, 255),
-                                           (7, 100, 1500, 3, 1), (8, 96, 3000, 5, 4), (2, 1, 1, 1, 1)])
+                                           (7, 100, 1500, 3, 1), (8, 96, 3000, 5, 4), (2, 1, 1, 1, 1),
+                                           (8, 128, 8000, 4, 31743), (8, 128, 8000, 4, 31744),
+                                           (4, 64, 500, 2, 40000)])
 def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
     """The CTA-pair SOS kernel (tcgen05 cta_group::2, M = 256, each CTA stages half
     of W's rows) and the single-CTA kernel give identical results, and both equal
-    the oracle: the pair only re-tiles the exact int32 contraction of Eq.(10)-(11)."""
+    the oracle: the pair only re-tiles the exact int32 contraction of Eq.(10)-(11).
+    gamma 31743 / 31744 at n_p = 1024 straddle the packed 16-bit epilogue's bound
+    (gamma + n_p < 0x7FFF); 40000 takes the 32-bit epilogue."""
     msgs = gbgen.messages(500 + c + l, m, c, l)
     net = make_net(gb, msgs, c, l)
     pr, _ = gbgen.probes(501 + c, msgs, 1537, e, l, random_count=5)
