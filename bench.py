@@ -237,6 +237,9 @@ def config_dict(args, cfg, ws):
             "seed": SEED}
 
 
+SM_COUNT, SM_CLOCK_GHZ = 148, 1.965   # B200 (B200_PROFILING.md); clocks sampled in the C3 line
+
+
 def run_store(args, cfg):
     """C5: storage scaling.  Step = gb_clear + gb_store(this rank's M/N messages) + NCCL MAX merge of
     W8 (uint8) + gb_seal.  Strong scaling: M fixed, sharded over the ranks."""
@@ -301,8 +304,14 @@ def run_store(args, cfg):
             "config": {"workload": desc, "c": c, "l": l, "M": m, "messages_per_gpu": hi - lo,
                        "edge_writes_per_message": c * (c - 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                         "traffic": None, "kernel": "store_kernel+seal_kernel",
-                         "note": "scattered u8 edge writes are L2-resident (W8 16 MiB); bytes = inputs + W8 + seal"},
+                         "traffic": None, "kernel": "store_priv_kernel+apply_kernel+seal_kernel",
+                         "note": "bytes = message input + W8 + seal; the store kernel is bound on chip by "
+                                 "shared-memory atomics (see smem_atomics)"},
+            "smem_atomics": {"bit_sets_per_s": (hi - lo) * c * (c - 1) / (ms / args.steps / 1e3),
+                             "ideal_per_s": SM_COUNT * 32 * SM_CLOCK_GHZ * 1e9,
+                             "frac": (hi - lo) * c * (c - 1) / (ms / args.steps / 1e3) / (SM_COUNT * 32 * SM_CLOCK_GHZ * 1e9),
+                             "note": "M*C*(C-1) random bit sets into shared-memory tiles vs one conflict-free "
+                                     "32-lane shared atomic per SM per clock (148 SMs, 1.965 GHz)"},
             "gpu_launches": net.launch_count() - l0}), flush=True)
     return 0
 

@@ -161,6 +161,7 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->queue);
     cudaFree(net->ovf);
     cudaFree(net->ovf_count);
+    cudaFree(net->spart);
     free(net);
     return GB_OK;
 }
@@ -190,7 +191,6 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream) {
     net->stored += m;
     if (loc == 1) {
         GB_CUDA(gb::launch_store(net, msgs, m, st), "gb_store: launch");
-        net->launches += 1;
         return GB_OK;
     }
     // Host messages: stage in chunks through device scratch (blocking).
@@ -203,7 +203,6 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream) {
         GB_CUDA(cudaMemcpyAsync(net->stage, msgs + s0 * net->s.C, (size_t)n * row,
                                 cudaMemcpyHostToDevice, st), "gb_store: H2D");
         GB_CUDA(gb::launch_store(net, (const uint16_t *)net->stage, n, st), "gb_store: launch");
-        net->launches += 1;
     }
     GB_CUDA(cudaStreamSynchronize(st), "gb_store: sync");
     return GB_OK;

@@ -63,12 +63,14 @@ struct gb_net {
     int64_t ovf_cap;
     unsigned long long *ovf_count;
     size_t vscratch_bytes;
+    uint32_t *spart;                       // per-chunk partial bit matrices of the privatised store
+    size_t spart_bytes;
 };
 
 namespace gb {
 
 // Launchers (return cudaError_t of the launch).
-cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
+cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
 bool decode_l2_supported(const Shape &s, int rule);

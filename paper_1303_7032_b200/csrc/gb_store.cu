@@ -12,6 +12,10 @@
 // Wb[i][w] (bit b = W8[i][32w+b]) with a warp ballot, and check the
 // invariants of Eq.(1): binary entries, w_ij = w_ji (L306), no intra-cluster
 // edge (L145), no padding edge.
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "gb_internal.h"
 
 namespace gb {
@@ -46,47 +50,232 @@ __global__ void store_kernel(Shape s, const uint16_t *__restrict__ msgs, int64_t
     }
 }
 
-// One warp per (row i, word w): lane b reads W8[i][32w+b], checks it, and the
-// warp ballot forms Wb[i][w].
+// One warp per 32x32 tile (rows i0.., columns j0..): lane r loads row i0+r of
+// the tile and row j0+r of the transposed tile (32 contiguous bytes each), packs
+// its row into Wb[i0+r][j0/32], and the warp checks the tile against the
+// transpose (32 ballots) and the structural invariants.
+__device__ __forceinline__ uint32_t pack32(const uint8_t *p, unsigned &nonbin) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(p);
+    const uint4 b = *reinterpret_cast<const uint4 *>(p + 16);
+    const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t bits = 0u;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        nonbin |= w[k] & 0xfefefefeu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bits |= ((w[k] >> (8 * q)) & 0xffu ? 1u : 0u) << (4 * k + q);
+    }
+    return bits;
+}
+
 __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *__restrict__ wb,
                             unsigned *__restrict__ dflag) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t total = (int64_t)s.np * s.nw;
-    if (warp >= total) return;
-    const int i = (int)(warp / s.nw);
-    const int w = (int)(warp - (int64_t)i * s.nw);
-    const int j = w * 32 + lane;
-    const unsigned v = w8[(int64_t)i * s.np + j];
-    unsigned bad = 0;
-    if (v > 1u) bad |= kFlagNotBinary;
-    if (v) {
-        const int ci = i / s.Lp, cj = j / s.Lp;
-        if (ci == cj) bad |= kFlagIntra;
-        if (i - ci * s.Lp >= s.L || j - cj * s.Lp >= s.L) bad |= kFlagPad;
+    const int nt = s.np / 32;
+    if (warp >= (int64_t)nt * nt) return;
+    const int ti = (int)(warp / nt), tj = (int)(warp - (int64_t)ti * nt);
+    const int i0 = 32 * ti, j0 = 32 * tj;
+    unsigned nonbin = 0u;
+    const uint32_t P = pack32(w8 + (int64_t)(i0 + lane) * s.np + j0, nonbin);   // W8[i0+lane][j0+b]
+    const uint32_t T = pack32(w8 + (int64_t)(j0 + lane) * s.np + i0, nonbin);   // W8[j0+lane][i0+b]
+    uint32_t R = 0u;                                                             // W8[j0+b][i0+lane]
+#pragma unroll 8
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t x = __ballot_sync(0xffffffffu, (T >> k) & 1u);
+        if (lane == k) R = x;
     }
-    if (w8[(int64_t)j * s.np + i] != v) bad |= kFlagAsym;
-    const unsigned bits = __ballot_sync(0xffffffffu, v != 0u);
+    const int ci = i0 / s.Lp, cj = j0 / s.Lp;
+    const int cb = j0 - cj * s.Lp;   // first column slot of the tile inside cluster cj
+    const uint32_t realc = cb >= s.L ? 0u : (s.L - cb >= 32 ? 0xffffffffu : ((1u << (s.L - cb)) - 1u));
+    const bool realr = (i0 + lane - ci * s.Lp) < s.L;
+    unsigned bad = nonbin ? kFlagNotBinary : 0u;
+    if (P != R) bad |= kFlagAsym;
+    if (P && ci == cj) bad |= kFlagIntra;
+    if ((P & ~realc) || (P && !realr)) bad |= kFlagPad;
+    wb[(int64_t)(i0 + lane) * s.nw + tj] = P;
     const unsigned anybad = __reduce_or_sync(0xffffffffu, bad);
-    if (lane == 0) {
-        wb[(int64_t)i * s.nw + w] = bits;
-        if (anybad) atomicOr(dflag, anybad);
+    if (lane == 0 && anybad) atomicOr(dflag, anybad);
+}
+
+// ---- privatised store (large m): one CTA = (row cluster c, column-cluster
+// group g, message chunk).  The CTA ORs the clique edges of its chunk that
+// fall in rows (c, *) x columns of group g into a bit tile in shared memory
+// (shared-memory atomics instead of scattered L2 byte writes), then writes the
+// tile into partial bit matrix `chunk`; apply_kernel ORs the partials into W8.
+// Every tile of every chunk writes its whole region (the c' = c block as
+// zeros), so the partials need no clearing.  Same edges as store_kernel:
+// W8[(c,m_c)][(c',m_c')] for every ordered pair c != c' (Eq.(1)).
+struct PrivPlan {
+    int G;        // column clusters per tile
+    int ngroups;  // ceil(C / G)
+    int tiles;    // C * ngroups
+    int chunks;
+    int64_t per_chunk;
+    size_t tile_bytes;
+};
+
+template <int NV>
+__global__ void __launch_bounds__(1024, 1)
+store_priv_kernel(Shape s, const uint16_t *__restrict__ msgs, int64_t m, int G, int ngroups, int tiles,
+                  int64_t per_chunk, uint32_t *__restrict__ part, unsigned long long *__restrict__ dcount,
+                  unsigned *__restrict__ dflag) {
+    extern __shared__ __align__(16) uint32_t tile[];
+    const int chunk = blockIdx.x / tiles;
+    const int t = blockIdx.x - chunk * tiles;
+    const int c = t / ngroups;
+    const int g0 = (t - c * ngroups) * G;
+    const int g1 = min(s.C, g0 + G);
+    const int tw = (g1 - g0) * s.Wc;                 // words per tile row
+    // odd row stride: with tw a multiple of 32 every row would start on bank 0, and the
+    // lanes of a warp (same column cluster at the same step) would share 8 banks
+    const int ts = tw | 1;
+    const int nwords = s.Lp * tw;
+    for (int i = threadIdx.x; i < s.Lp * ts; i += blockDim.x) tile[i] = 0u;
+    __syncthreads();
+    const int64_t b = (int64_t)chunk * per_chunk;
+    const int64_t e = min(m, b + per_chunk);
+    const bool counter = (t == 0);
+    for (int64_t mi = b + threadIdx.x; mi < e; mi += blockDim.x) {
+        const uint16_t *row = msgs + mi * s.C;
+        unsigned mc, sy[NV > 0 ? 8 * NV : 1];
+        bool ok = true;
+        if constexpr (NV > 0) {
+            // the message as NV 16-byte vectors (C = 8*NV, rows 16-byte aligned)
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4 *>(row) + v);
+                const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    sy[8 * v + 2 * h] = w4[h] & 0xffffu;
+                    sy[8 * v + 2 * h + 1] = w4[h] >> 16;
+                }
+            }
+            mc = 0;
+#pragma unroll
+            for (int cc = 0; cc < 8 * NV; ++cc) {
+                ok &= (sy[cc] < (unsigned)s.L);
+                if (cc == c) mc = sy[cc];
+            }
+        } else {
+            for (int cc = 0; cc < s.C; ++cc) ok &= (__ldg(row + cc) < s.L);
+            mc = ok ? __ldg(row + c) : 0u;
+        }
+        if (!ok) {
+            if (counter) {
+                atomicAdd(dcount, 1ull);
+                atomicOr(dflag, kFlagStoreInvalid);
+            }
+            continue;
+        }
+        uint32_t *trow = tile + mc * ts;
+        if constexpr (NV > 0) {
+#pragma unroll
+            for (int cc = 0; cc < 8 * NV; ++cc) {
+                if (cc == c || cc < g0 || cc >= g1) continue;
+                const int col = (cc - g0) * s.Lp + (int)sy[cc];
+                atomicOr(trow + (col >> 5), 1u << (col & 31));
+            }
+        } else {
+            for (int cc = g0; cc < g1; ++cc) {
+                if (cc == c) continue;
+                const int col = (cc - g0) * s.Lp + __ldg(row + cc);
+                atomicOr(trow + (col >> 5), 1u << (col & 31));
+            }
+        }
     }
+    __syncthreads();
+    uint32_t *dst = part + (size_t)chunk * s.np * s.nw + (size_t)c * s.Lp * s.nw + g0 * s.Wc;
+    for (int i = threadIdx.x; i < nwords; i += blockDim.x) {
+        const int r = i / tw, w = i - r * tw;
+        dst[(size_t)r * s.nw + w] = tile[r * ts + w];
+    }
+}
+
+// One thread per (row i, word w) of the bit matrix: OR the chunk partials and
+// set the corresponding W8 bytes (read-modify-write of 32 bytes only when some
+// bit is set; W8 keeps every edge it already had).
+__global__ void apply_kernel(Shape s, const uint32_t *__restrict__ part, int chunks, uint8_t *__restrict__ w8) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t total = (int64_t)s.np * s.nw;
+    if (idx >= total) return;
+    uint32_t bits = 0u;
+    for (int ch = 0; ch < chunks; ++ch) bits |= __ldg(part + (size_t)ch * total + idx);
+    if (!bits) return;
+    const int64_t i = idx / s.nw, w = idx - i * s.nw;
+    uint4 *p = reinterpret_cast<uint4 *>(w8 + i * s.np + w * 32);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint4 v = p[h];
+        uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t nib = (bits >> (16 * h + 4 * k)) & 15u;
+            q[k] |= (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+        }
+        p[h] = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+}
+
+constexpr size_t kPrivTileMax = 128 * 1024;
+
+PrivPlan priv_plan(const Shape &s, int64_t m, int sm_count) {
+    PrivPlan p;
+    const size_t blk = (size_t)s.Lp * s.Lp / 8;      // one cluster-pair block in bits
+    p.G = (int)std::min<size_t>((size_t)s.C, std::max<size_t>(1, kPrivTileMax / blk));
+    p.ngroups = (s.C + p.G - 1) / p.G;
+    p.tiles = s.C * p.ngroups;
+    p.tile_bytes = (size_t)p.G * blk + (size_t)s.Lp * 4;   // + one pad word per row
+    const int resident = (int)std::max<size_t>(1, std::min<size_t>(8, (200 * 1024) / p.tile_bytes));
+    const int64_t slots = std::max<int64_t>(1, (int64_t)sm_count * resident / p.tiles);
+    const int64_t want = std::max<int64_t>(1, (m + 4095) / 4096);
+    p.chunks = (int)std::min<int64_t>(slots, want);
+    p.per_chunk = (m + p.chunks - 1) / p.chunks;
+    return p;
 }
 
 }  // namespace
 
-cudaError_t launch_store(const gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st) {
-    const int64_t threads = m * net->s.C;
-    const int block = 256;
-    const int64_t grid = (threads + block - 1) / block;
-    store_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, msgs, m, net->w8, net->dcount,
-                                                   net->dflag);
+cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st) {
+    const Shape &s = net->s;
+    // small batches: scattered relaxed byte stores (no tile setup / apply pass)
+    if (m * s.C * (s.C - 1) < (int64_t)s.np * s.nw * 8 || getenv("GB_STORE_SCATTER")) {
+        const int64_t threads = m * s.C;
+        const int block = 256;
+        const int64_t grid = (threads + block - 1) / block;
+        store_kernel<<<(unsigned)grid, block, 0, st>>>(s, msgs, m, net->w8, net->dcount, net->dflag);
+        net->launches += 1;
+        return cudaGetLastError();
+    }
+    const PrivPlan p = priv_plan(s, m, net->sm_count);
+    const size_t need = (size_t)p.chunks * s.np * s.nw * sizeof(uint32_t);
+    if (net->spart_bytes < need) {
+        cudaFree(net->spart);
+        net->spart = nullptr;
+        net->spart_bytes = 0;
+        if (cudaMalloc(&net->spart, need) != cudaSuccess) {
+            cudaGetLastError();
+            return cudaErrorMemoryAllocation;
+        }
+        net->spart_bytes = need;
+    }
+    // vector loads of whole messages when C = 8, 16, 24, 32 and rows are 16-byte aligned
+    const int nv = ((s.C % 8) == 0 && s.C <= 32 && ((uintptr_t)msgs & 15u) == 0) ? s.C / 8 : 0;
+    auto fn = nv == 1 ? store_priv_kernel<1> : nv == 2 ? store_priv_kernel<2>
+            : nv == 3 ? store_priv_kernel<3> : nv == 4 ? store_priv_kernel<4> : store_priv_kernel<0>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_bytes);
+    if (e != cudaSuccess) return e;
+    fn<<<(unsigned)(p.chunks * p.tiles), 1024, p.tile_bytes, st>>>(
+        s, msgs, m, p.G, p.ngroups, p.tiles, p.per_chunk, net->spart, net->dcount, net->dflag);
+    const int64_t total = (int64_t)s.np * s.nw;
+    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, net->spart, p.chunks, net->w8);
+    net->launches += 2;
     return cudaGetLastError();
 }
 
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st) {
-    const int64_t warps = (int64_t)net->s.np * net->s.nw;
+    const int64_t warps = (int64_t)(net->s.np / 32) * (net->s.np / 32);
     const int block = 256;
     const int64_t grid = (warps * 32 + block - 1) / block;
     seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dflag);

@@ -76,6 +76,84 @@ def test_store_matches_oracle(gb, c, l, m):
     assert net.info() == (c, l, net.n_padded, m)
 
 
+@pytest.mark.parametrize("c,l,m", [(8, 128, 20000), (16, 512, 60000), (5, 33, 5000), (64, 32, 3000),
+                                   (3, 100, 5000), (16, 256, 300000)])
+@pytest.mark.parametrize("path", ["privatised", "scatter"])
+def test_store_paths_match_oracle(gb, monkeypatch, c, l, m, path):
+    """Both store kernels (shared-memory bit tiles + apply pass for large
+    batches; scattered byte stores, forced with GB_STORE_SCATTER) give the
+    oracle's W (Eq.(1)) byte for byte, accumulate over calls (OR),
+    and skip + count messages holding a symbol >= L (reading R21)."""
+    if path == "scatter":
+        monkeypatch.setenv("GB_STORE_SCATTER", "1")
+    else:
+        monkeypatch.delenv("GB_STORE_SCATTER", raising=False)
+    msgs = gbgen.messages(77 + m + c, m, c, l)
+    bad = msgs[:5].copy()
+    bad[0, c - 1] = l
+    bad[1, 0] = 0xFFFF
+    bad[2, c // 2] = 0xFFFE
+    allm = np.concatenate([msgs[: m // 3], bad[:3], msgs[m // 3:]])
+    net = gb.Net(c, l)
+    net.store(to_dev(allm[: len(allm) // 2]))
+    net.store(to_dev(allm[len(allm) // 2:]))
+    with pytest.raises(gb.GBError) as ei:
+        net.seal()
+    assert ei.value.code == gb.GB_EINVAL and "3 stored message" in str(ei.value)
+    w, _ = oracle.store(msgs, c, l)
+    np.testing.assert_array_equal(net.weights().cpu().numpy(), padded_w(w, c, l))
+    net.close()
+
+
+@pytest.mark.parametrize("c,l", [(5, 33), (16, 256), (3, 3)])
+def test_seal_invariants_every_tile(gb, c, l):
+    """gb_seal checks Eq.(1)'s structure (binary entries, w_ij = w_ji P:L306,
+    no intra-cluster edge P:L145, no padding edge) on every 32x32 tile: an
+    edit anywhere in W8 is caught; the packed rows equal W8 (decode parity)."""
+    msgs = gbgen.messages(3, 400, c, l)
+    w, _ = oracle.store(msgs, c, l)
+    net = make_net(gb, msgs, c, l)
+    w8 = net.weights()
+    np_ = net.n_padded
+    lp = np_ // c
+    rng = np.random.default_rng(c * 1000 + l)
+    real = [cc * lp + x for cc in range(c) for x in range(l)]
+    for _ in range(6):
+        i, j = (int(v) for v in rng.choice(real, 2))
+        if i // lp == j // lp:
+            continue
+        old = int(w8[i, j])
+        w8[i, j] = 1 - old                       # asymmetric
+        with pytest.raises(gb.GBError, match="asymmetric"):
+            net.seal()
+        w8[j, i] = 1 - old                       # symmetric again: fine
+        net.seal()
+        w8[i, j] = old
+        w8[j, i] = old
+        w8[i, j] = 2
+        w8[j, i] = 2                             # symmetric but not binary
+        with pytest.raises(gb.GBError, match="non-binary"):
+            net.seal()
+        w8[i, j] = old
+        w8[j, i] = old
+    net.seal()
+    if l < lp:                                   # padding neuron of the last cluster
+        p_, q = (c - 1) * lp + l, int(real[0])
+        w8[p_, q] = 1
+        w8[q, p_] = 1
+        with pytest.raises(gb.GBError, match="padding"):
+            net.seal()
+        w8[p_, q] = 0
+        w8[q, p_] = 0
+    d = int(real[-1])
+    w8[d, d] = 1                                 # diagonal = intra-cluster
+    with pytest.raises(gb.GBError, match="intra-cluster"):
+        net.seal()
+    w8[d, d] = 0
+    net.seal()
+    np.testing.assert_array_equal(w8.cpu().numpy(), padded_w(w, c, l))
+
+
 def test_sharded_store_max_merge_equals_single(gb):
     """W of a sharded store merged by MAX on uint8 (= OR on
     {0,1}) equals the single-device W byte for byte."""
