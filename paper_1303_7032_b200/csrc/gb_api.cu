@@ -324,6 +324,7 @@ const char *gb_decode_kernel(gb_net *net, int rule) {
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
         return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
+    if (rule == GB_HYBRID && gb::decode_hyb8_supported(net->s, rule, 0, nullptr)) return "decode_hyb8_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule)) return "decode_l2_kernel";
     return "decode_generic_kernel";

@@ -80,6 +80,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
     uint32_t *X = smem + np * nw;                   // [MAXS*WC][threads]
     uint32_t *Z = X + (MAXS == 4 ? 0 : MAXS * WC * NT);   // one all-zero block
     const int tid = threadIdx.x;
+    if (list && *list_count == 0ull) return;   // no queued probe: skip the W load
     const uint32_t w_s = (uint32_t)__cvta_generic_to_shared(W);
     const uint32_t zaddr = (uint32_t)__cvta_generic_to_shared(Z);
     if (tid < 4) Z[tid] = 0u;
@@ -454,8 +455,12 @@ cudaError_t launch_rule(gb_net *net, const uint16_t *probes, int64_t k, int max_
     }
     cudaError_t e = cudaMemsetAsync(net->ovf_count, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    e = launch_t<WC, RULE, 4, kNarrowThreads>(net, probes, k, max_iters, state, iters, status, nullptr, nullptr,
-                                              net->ovf, net->ovf_count, st);
+    e = cudaErrorNotSupported;
+    if (WC == 4 && RULE == GB_HYBRID && decode_hyb8_supported(net->s, RULE, k, state))
+        e = launch_decode_hyb8(net, probes, k, max_iters, state, iters, status, st);
+    if (e == cudaErrorNotSupported)   // other shapes, or no tensor map for this output buffer
+        e = launch_t<WC, RULE, 4, kNarrowThreads>(net, probes, k, max_iters, state, iters, status, nullptr, nullptr,
+                                                  net->ovf, net->ovf_count, st);
     if (e != cudaSuccess) return e;
     return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, net->ovf,
                                                net->ovf_count, nullptr, nullptr, st);

@@ -86,6 +86,11 @@ bool sos_2cta_enabled(const Shape &s);
 int sos_2cta_box_rows(const Shape &s);
 cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, int64_t k, int max_iters,
                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+// C = 8, Wc = 4 hybrid decode of the probes with e <= 4 (gb_decode_hyb8.cu); the
+// others are appended to net->ovf.
+bool decode_hyb8_supported(const Shape &s, int rule, int64_t k, const void *state);
+cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                               uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,

@@ -154,6 +154,40 @@ def test_seal_invariants_every_tile(gb, c, l):
     np.testing.assert_array_equal(w8.cpu().numpy(), padded_w(w, c, l))
 
 
+@pytest.mark.parametrize("l,m,k", [(128, 20000, 3001), (100, 5000, 777), (97, 12000, 31), (128, 0, 64),
+                                   (128, 30000, 1)])
+def test_hyb8_matches_oracle_and_generic(gb, monkeypatch, l, m, k):
+    """The C=8 hybrid kernel (staged push, TMA-stored output) against the
+    oracle and against the generic shared-memory kernel (GB_NO_HYB8): ragged
+    batch (k not a multiple of 32, k < 32), every erasure count 0..8 (e > 4
+    goes to the wide-slot kernel), invalid probes, random non-stored probes."""
+    c = 8
+    msgs = gbgen.messages(900 + l + m, max(m, 1), c, l)[:m]
+    pr, _ = gbgen.probes(901 + k, msgs if m else gbgen.messages(5, 10, c, l), k, 4, l, random_count=k // 5)
+    rng = np.random.default_rng(k + l)
+    for i in range(0, k, 3):                      # mixed erasure counts per probe
+        e = int(rng.integers(0, c + 1))
+        row = gbgen.messages(1000 + i, 1, c, l)[0] if rng.random() < 0.5 else pr[i].copy()
+        row[row == 0xFFFF] = rng.integers(0, l)
+        row[rng.choice(c, e, replace=False)] = 0xFFFF
+        pr[i] = row
+    if k > 10:
+        pr[5, 2] = l                                 # invalid symbol
+        pr[7, 0] = 0xFFFE
+    w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
+    net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(2) == "decode_hyb8_kernel"
+    want = oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=20)
+    got = gpu_decode(net, pr, 2, 1, 20)
+    assert_same(got, want, 2, f"hyb8 l={l} m={m} k={k}")
+    monkeypatch.setenv("GB_NO_HYB8", "1")
+    assert_same(gpu_decode(net, pr, 2, 1, 20), want, 2, "generic")
+    assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "T=3")
+    monkeypatch.delenv("GB_NO_HYB8")
+    assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "hyb8 T=3")
+    net.close()
+
+
 def test_sharded_store_max_merge_equals_single(gb):
     """W of a sharded store merged by MAX on uint8 (= OR on
     {0,1}) equals the single-device W byte for byte."""
@@ -368,7 +402,7 @@ def test_determinism(gb):
 @pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc2_kernel"), (16, 256, 0, "sos_tc_kernel"),
                                            (4, 16, 0, "sos_tc2_kernel"), (3, 3, 0, "sos_tc2_kernel"),
                                            (8, 256, 0, "sos_tc_kernel"), (4, 256, 0, "sos_tc2_kernel"),
-                                           (8, 128, 2, "decode_smem_kernel"), (8, 128, 1, "decode_smem_kernel"),
+                                           (8, 128, 2, "decode_hyb8_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
                                            (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2_kernel"),

@@ -10,7 +10,7 @@ cat gpurun_out/bench_full_$TAG.json
 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$TAG.json 2>&1
 tail -1 gpurun_out/bench_ref_$TAG.json
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_smem -s 3 -c 1 -o gpurun_out/prof_hyb_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_hyb8 -s 2 -c 1 -o gpurun_out/prof_hyb_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:decode_l2 -s 3 -c 1 -o gpurun_out/prof_l2_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c4 --rule 1 --probes 100000 > /dev/null 2>&1
 rm -f gpurun_out/bench_rules_$TAG.jsonl
