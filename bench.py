@@ -39,7 +39,7 @@ CONFIGS = {
     "c2": (8, 128, 5000, 4, 2, 100_000, "BASELINE C2 point: c=8 l=128 M=5k e=4, 10^5 probes"),
     "c1": (4, 16, 50, 2, 2, 1000, "BASELINE C1: c=4 l=16 M=50 e=2, 1000 probes"),
     "c4": (16, 256, 100000, 8, 1, 1_000_000, "BASELINE C4: c=16 l=256 M=100k e=8, 10^6 probes"),
-    "c5": (16, 256, 10_000_000, 0, -1, 0, "BASELINE C5: store of 10^7 messages at c=16 l=256 (sharded, NCCL MAX merge)"),
+    "c5": (16, 256, 10_000_000, 0, -1, 0, "BASELINE C5: store of 10^7 messages at c=16 l=256 (sharded over ranks, partial W merged over NCCL)"),
     # the paper's Scenario 2: its only published runtime (14.86 s for
     # 30000 probes on a Tesla C1060 => 2019 probes/s) is quoted as vs_baseline context.
     "s2": (16, 512, 50000, 7, 2, 30000, "Scenario 2 (PAPER.md L731): c=16 l=512 M=50k e=7 hybrid, 30000 probes"),
@@ -278,14 +278,15 @@ def run_store(args, cfg):
     shard = torch.from_numpy(np.ascontiguousarray(msgs[lo:hi]).view(np.int16)).to(dev)
     net = gb.Net(c, l, device=local)
     stream = torch.cuda.current_stream()
+    store_step = gdist.sharded_store_bits if args.merge == "bits" else gdist.sharded_store
     for _ in range(args.warmup):
-        gdist.sharded_store(net, shard)
+        store_step(net, shard)
     torch.cuda.synchronize()
     l0 = net.launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(args.steps):
-        gdist.sharded_store(net, shard)
+        store_step(net, shard)
     b.record(stream)
     torch.cuda.synchronize()
     ms = gdist.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
@@ -302,7 +303,9 @@ def run_store(args, cfg):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (gbgen, seed 0x5EED)",
             "config": {"workload": desc, "c": c, "l": l, "M": m, "messages_per_gpu": hi - lo,
-                       "edge_writes_per_message": c * (c - 1)},
+                       "edge_writes_per_message": c * (c - 1),
+                       "merge": ("all-gather of packed partial W + gb_or_bits" if args.merge == "bits"
+                                 else "all-reduce MAX of u8 W8") if ws > 1 else "none (1 rank)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "kernel": "store_priv_kernel+apply_kernel+seal_kernel",
                          "note": "bytes = message input + W8 + seal; the store kernel is bound on chip by "
@@ -327,6 +330,8 @@ def main():
     ap.add_argument("--messages", type=int, default=None)
     ap.add_argument("--probes", type=int, default=None)
     ap.add_argument("--gamma", type=int, default=2)
+    ap.add_argument("--merge", default="bits", choices=["bits", "max"],
+                    help="C5 store merge over ranks: packed all-gather + OR (N3) or u8 MAX all-reduce")
     ap.add_argument("--max-iters", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=12.0)

@@ -112,6 +112,28 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
 int gb_weights(gb_net *net, uint8_t **w8, int64_t *nbytes);
 
 /*
+ * gb_bits -- expose the library-owned packed rows Wb (n_padded x n_padded/32
+ * uint32, bit b of word w of row i = w_{i,32w+b}), valid after a successful
+ * gb_seal and until the next gb_store / gb_clear / gb_or_bits / W8 edit.
+ * This is the compact form for merging sharded stores:
+ * all-gather the ranks' Wb (8x fewer bytes than the u8 W8) and OR them in
+ * with gb_or_bits.  *wb is a device pointer.  Returns GB_ESTATE if unsealed.
+ */
+int gb_bits(gb_net *net, uint32_t **wb, int64_t *nbytes);
+
+/*
+ * gb_or_bits -- OR `count` packed bit matrices (device pointer to count
+ * consecutive n_padded x n_padded/32 uint32 matrices in the gb_bits layout)
+ * into W8: w_ij |= bit (i, j) of any of them.  Eq.(1) is an OR of cliques
+ * (PAPER.md L149-153), so OR-ing the partial W's of message shards gives the
+ * W of the whole message set.  Unseals; stream-ordered.  count == 0 is a
+ * no-op; GB_EINVAL for count < 0 or NULL bits.  A matrix that breaks Eq.(1)'s
+ * structure (asymmetric, intra-cluster or padding bits) is reported by the
+ * next gb_seal.
+ */
+int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream);
+
+/*
  * gb_seal -- freeze W for retrieval ("At the retrieval stage,
  * the variables w are fixed"): pack W8 into bit rows (the B200 counterpart of
  * the compressed W' of L381 / Alg. 2 line 6) and check the structural

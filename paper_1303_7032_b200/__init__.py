@@ -28,7 +28,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB: experiment builds
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
-EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_seal",
+EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_bits", "gb_or_bits", "gb_seal",
            "gb_decode", "gb_info", "gb_launch_count", "gb_decode_kernel", "gb_last_error",
            "gb_version")
 
@@ -58,6 +58,8 @@ def lib() -> ctypes.CDLL:
         "gb_store": ([P, P, i64, P], i32),
         "gb_weights": ([P, PP, ctypes.POINTER(i64)], i32),
         "gb_seal": ([P, P], i32),
+        "gb_bits": ([P, PP, ctypes.POINTER(i64)], i32),
+        "gb_or_bits": ([P, P, i64, P], i32),
         "gb_decode": ([P, P, i64, i32, i32, i32, P, P, P, P], i32),
         "gb_info": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                      ctypes.POINTER(i64)], i32),
@@ -148,6 +150,22 @@ class Net:
         _check(lib().gb_weights(self._h, ctypes.byref(p), ctypes.byref(nb)))
         arr = _CudaArray(p.value, (self.n_padded, self.n_padded), "|u1")
         return torch.as_tensor(arr, device=f"cuda:{self.device}")
+
+    def bits(self):
+        """The library-owned packed rows Wb as a torch int32 cuda tensor [n_p, nw]
+        (no copy; valid after seal until W changes)."""
+        import torch
+        p = ctypes.c_void_p()
+        nb = ctypes.c_int64()
+        _check(lib().gb_bits(self._h, ctypes.byref(p), ctypes.byref(nb)))
+        arr = _CudaArray(p.value, (self.n_padded, self.nw), "<i4")
+        return torch.as_tensor(arr, device=f"cuda:{self.device}")
+
+    def or_bits(self, bits, stream=None):
+        """gb_or_bits: OR packed bit matrices ([count, n_p, nw] int32 cuda tensor) into W8."""
+        assert bits.is_cuda and bits.is_contiguous() and tuple(bits.shape[-2:]) == (self.n_padded, self.nw)
+        count = bits.numel() // (self.n_padded * self.nw)
+        _check(lib().gb_or_bits(self._h, ctypes.c_void_p(bits.data_ptr()), count, _stream(stream)))
 
     def info(self):
         c, l, n, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()

@@ -215,6 +215,26 @@ int gb_weights(gb_net *net, uint8_t **w8, int64_t *nbytes) {
     return GB_OK;
 }
 
+int gb_bits(gb_net *net, uint32_t **wb, int64_t *nbytes) {
+    if (!net) return fail(GB_EINVAL, "gb_bits: net is NULL");
+    if (!net->sealed) return fail(GB_ESTATE, "gb_bits: network not sealed (Wb is built by gb_seal)");
+    if (wb) *wb = net->wb;
+    if (nbytes) *nbytes = (int64_t)net->s.np * net->s.nw * (int64_t)sizeof(uint32_t);
+    return GB_OK;
+}
+
+int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream) {
+    if (!net) return fail(GB_EINVAL, "gb_or_bits: net is NULL");
+    if (count < 0) return fail(GB_EINVAL, "gb_or_bits: count = %lld < 0", (long long)count);
+    if (count == 0) return GB_OK;
+    if (!bits) return fail(GB_EINVAL, "gb_or_bits: bits is NULL");
+    DeviceGuard g(net->device);
+    if (where(bits, net->device) != 1) return fail(GB_EINVAL, "gb_or_bits: bits must be device memory of the handle's device");
+    net->sealed = false;
+    GB_CUDA(gb::launch_or_bits(net, bits, count, (cudaStream_t)stream), "gb_or_bits: launch");
+    return GB_OK;
+}
+
 int gb_seal(gb_net *net, void *stream) {
     if (!net) return fail(GB_EINVAL, "gb_seal: net is NULL");
     DeviceGuard g(net->device);

@@ -72,6 +72,7 @@ namespace gb {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
+cudaError_t launch_or_bits(gb_net *net, const uint32_t *bits, int64_t count, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
 bool decode_l2_supported(const Shape &s, int rule);
 cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,

@@ -274,6 +274,14 @@ cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStrea
     return cudaGetLastError();
 }
 
+// OR `count` packed bit matrices into W8 (the apply pass of the privatised store).
+cudaError_t launch_or_bits(gb_net *net, const uint32_t *bits, int64_t count, cudaStream_t st) {
+    const int64_t total = (int64_t)net->s.np * net->s.nw;
+    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(net->s, bits, (int)count, net->w8);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
 cudaError_t launch_seal(const gb_net *net, cudaStream_t st) {
     const int64_t warps = (int64_t)(net->s.np / 32) * (net->s.np / 32);
     const int block = 256;

@@ -11,6 +11,10 @@ box, gloo in the CPU tests).  Nothing here computes any part of the method:
   all-reduce MAX on uint8 (MAX over {0,1} is OR; Eq.(1) is an OR of
   cliques).  MAX must never be applied to packed bit
   words (max(0b01, 0b10) = 0b10 != 0b11), so the merge takes the u8 matrix;
+* or the partials are exchanged packed: each rank seals its
+  partial W (bit rows Wb, n_p^2/8 bytes), the Wb's are all-gathered, and every
+  rank ORs all of them into its W8 (gb_or_bits) -- per rank (G-1) n_p^2/8 bytes
+  received instead of the ring all-reduce's 2 (G-1)/G n_p^2 bytes of u8;
 * alternatively W is built once and replicated with a broadcast.
 """
 from __future__ import annotations
@@ -79,4 +83,33 @@ def sharded_store(net, msgs_shard, group=None, stream=None):
     if msgs_shard.shape[0]:
         net.store(msgs_shard, stream)
     merge_weights_(net.weights(), group)
+    net.seal(stream)
+
+
+def gather_bits(wb: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather this rank's packed rows Wb [n_p, nw] (int32) into [G, n_p, nw]."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return wb.unsqueeze(0).contiguous()
+    ws = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((ws,) + tuple(wb.shape), dtype=wb.dtype, device=wb.device)
+        dist.all_gather_into_tensor(out, wb.contiguous(), group=group)
+        return out
+    # gloo (CPU tests, and the one-GPU test hook GB_DIST_BACKEND=gloo): host round trip
+    src = wb.detach().cpu().contiguous()
+    out = torch.empty((ws,) + tuple(src.shape), dtype=src.dtype)
+    dist.all_gather(list(out.unbind(0)), src, group=group)
+    return out.to(wb.device)
+
+
+def sharded_store_bits(net, msgs_shard, group=None, stream=None):
+    """gb_clear + gb_store(shard) + gb_seal (pack the partial) + all-gather of
+    the packed partials + gb_or_bits + gb_seal on one rank (N3 merge)."""
+    net.clear(stream)
+    if msgs_shard.shape[0]:
+        net.store(msgs_shard, stream)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        net.seal(stream)
+        allb = gather_bits(net.bits(), group)
+        net.or_bits(allb, stream)
     net.seal(stream)

@@ -3,7 +3,8 @@
 The GPU store/decode are replaced by the CPU oracle (test-only), so what is
 tested is the sharding and merge logic of paper_1303_7032_b200.dist:
   * the MAX all-reduce of per-rank partial W (uint8) equals the single-store
-    W byte for byte (Eq.(1) OR semantics, SURVEY §8.e);
+    W byte for byte (Eq.(1) OR semantics), and so does the OR of
+    the all-gathered packed partials (gather_bits, SURVEY §8.f N3);
   * decoding per-rank probe shards and gathering equals decoding the whole
     batch (Eq.(11) column independence), for the weak
     (per-rank K) and strong (split K) shardings;
@@ -45,6 +46,13 @@ def _worker(rank, ws, port, out_dir):
         assert np.array_equal(w8.numpy(), full), "MAX merge != single store"
         with pytest.raises(TypeError):
             gdist.merge_weights_(torch.zeros(4, dtype=torch.int32))
+        # N3 packed merge: all-gather of the packed partials, OR == single store
+        packed = np.packbits(part, axis=1, bitorder="little").view(np.int32)   # Wb layout (n = 256)
+        allb = gdist.gather_bits(torch.from_numpy(packed.copy()))
+        assert tuple(allb.shape) == (ws,) + packed.shape
+        ored = np.bitwise_or.reduce(allb.numpy().view(np.uint32), axis=0)
+        unpacked = np.unpackbits(ored.view(np.uint8), axis=1, bitorder="little")
+        assert np.array_equal(unpacked, full), "OR of gathered packed partials != single store"
         # weak sharding: each rank decodes k probes of the global stream
         k = 64
         lo, hi = gdist.weak_bounds(k, rank)

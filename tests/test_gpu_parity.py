@@ -188,6 +188,38 @@ def test_hyb8_matches_oracle_and_generic(gb, monkeypatch, l, m, k):
     net.close()
 
 
+def test_or_bits_merge_equals_single(gb):
+    """OR-ing the packed partial W's (gb_bits of each shard's
+    sealed net, stacked) into an empty net with gb_or_bits gives the W of the
+    whole message set (Eq.(1) is an OR of cliques); plus argument errors."""
+    for c, l, m in ((8, 128, 20000), (5, 33, 3000), (16, 256, 100000)):
+        msgs = gbgen.messages(15 + c, m, c, l)
+        whole = make_net(gb, msgs, c, l)
+        parts = [make_net(gb, msgs[i::3], c, l) for i in range(3)]
+        stacked = torch.stack([p_.bits() for p_ in parts]).contiguous()
+        fresh = gb.Net(c, l)
+        fresh.or_bits(stacked)
+        fresh.seal()
+        assert torch.equal(fresh.weights(), whole.weights())
+        assert torch.equal(fresh.bits(), whole.bits())
+        # OR into a net that already holds a shard (accumulates)
+        parts[0].or_bits(stacked[1:].contiguous())
+        parts[0].seal()
+        assert torch.equal(parts[0].weights(), whole.weights())
+        for n in parts + [whole, fresh]:
+            n.close()
+    net = gb.Net(4, 16)
+    with pytest.raises(gb.GBError) as ei:
+        net.bits()
+    assert ei.value.code == gb.GB_ESTATE
+    assert gb.lib().gb_or_bits(net._h, None, 1, None) == gb.GB_EINVAL
+    assert gb.lib().gb_or_bits(net._h, None, -1, None) == gb.GB_EINVAL
+    assert gb.lib().gb_or_bits(net._h, None, 0, None) == gb.GB_OK
+    host = np.zeros((net.n_padded, net.nw), np.uint32)
+    assert gb.lib().gb_or_bits(net._h, host.ctypes.data, 1, None) == gb.GB_EINVAL
+    net.close()
+
+
 def test_sharded_store_max_merge_equals_single(gb):
     """W of a sharded store merged by MAX on uint8 (= OR on
     {0,1}) equals the single-device W byte for byte."""
