@@ -743,30 +743,53 @@ bool sos_tc2_supported(const Shape &s) {
     return plan2(s, 1, P, smem);
 }
 
+// W8g = W8 + gamma*I (the B operand of the warp-specialised kernels), rebuilt after a
+// seal or a gamma change; gamma > 255 is added in the epilogue instead (B stays W8).
+static cudaError_t ensure_w8g(gb_net *net, int gamma, cudaStream_t st) {
+    if (!net->w8g) {
+        if (cudaMalloc(&net->w8g, (size_t)net->s.np * net->s.np) != cudaSuccess) {
+            cudaGetLastError();
+            net->w8g = nullptr;
+            return cudaErrorMemoryAllocation;
+        }
+        net->w8g_gen = ~0ull;
+    }
+    const int gfold = gamma > 255 ? 0 : gamma;
+    if (net->w8g_gen != net->seal_gen || net->w8g_gamma != gfold) {
+        diag_kernel<<<net->sm_count * 4, 256, 0, st>>>(net->s, net->w8, net->w8g, gfold);
+        net->launches += 1;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+        net->w8g_gen = net->seal_gen;
+        net->w8g_gamma = gfold;
+    }
+    return cudaSuccess;
+}
+
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     Sos2Params P2;
     size_t smem2;
+    if (sos_tc3_enabled(net->s)) {   // 1024 < n_p <= 4096: streamed A tile
+        cudaError_t e = ensure_w8g(net, gamma, st);
+        if (e != cudaSuccess) return e;
+        if (!net->wmap_g3_ok) {
+            alignas(8) unsigned char pb[64];
+            size_t smem3;
+            if (!plan3(net->s, gamma, pb, smem3)) return cudaErrorNotSupported;
+            net->wmap_g3_ok = sos_encode_map(net, net->w8g, plan3_box_rows(pb), net->wmap_g3);
+            if (!net->wmap_g3_ok) return cudaErrorNotSupported;
+        }
+        return launch_sos_tc3(net, gamma, net->wmap_g3, probes, k, max_iters, state, iters, status, st);
+    }
     if (plan2(net->s, gamma, P2, smem2) &&
         (net->s.Wc == 1 || net->s.Wc == 2 || net->s.Wc == 3 || net->s.Wc == 4 || net->s.Wc == 8)) {
-        // B operand W8 + gamma*I (rebuilt after each seal or gamma change)
-        if (!net->w8g) {
-            if (cudaMalloc(&net->w8g, (size_t)net->s.np * net->s.np) != cudaSuccess) {
-                cudaGetLastError();
-                net->w8g = nullptr;
-                return cudaErrorMemoryAllocation;
-            }
-            if (!sos_encode_map(net, net->w8g, P2.BR, net->wmap_g)) return cudaErrorNotSupported;
-            net->w8g_gen = ~0ull;
-        }
-        const int gfold = gamma > 255 ? 0 : gamma;
-        if (net->w8g_gen != net->seal_gen || net->w8g_gamma != gfold) {
-            diag_kernel<<<net->sm_count * 4, 256, 0, st>>>(net->s, net->w8, net->w8g, gfold);
-            net->launches += 1;
-            cudaError_t e = cudaGetLastError();
-            if (e != cudaSuccess) return e;
-            net->w8g_gen = net->seal_gen;
-            net->w8g_gamma = gfold;
+        const bool fresh = !net->w8g;
+        cudaError_t e = ensure_w8g(net, gamma, st);
+        if (e != cudaSuccess) return e;
+        if (fresh || !net->wmap_g_ok) {
+            net->wmap_g_ok = sos_encode_map(net, net->w8g, P2.BR, net->wmap_g);
+            if (!net->wmap_g_ok) return cudaErrorNotSupported;
         }
         if (sos_2cta_enabled(net->s)) {
             if (!net->wmap_g2_ok) {

@@ -1,0 +1,338 @@
+// gb_decode_sos_tc3.cu -- sum-of-sum decode on the tensor cores for networks
+// whose expanded A tile does not fit in shared memory (1024 < n_p <= 4096,
+// Lp <= 256; BASELINE C4: c=16 l=256, n_p = 4096).
+//
+// Same method and per-probe semantics as sos_tc2_kernel (gb_decode_sos_tc.cu):
+// a3 S^t = W V^t + gamma V^t as an exact int8 x int8 -> int32 contraction
+// (Eq.(3), Eq.(10)-(11) L328/L349, Alg. 1 line 4) with
+// tcgen05.mma.kind::i8 and TMEM accumulators; a4 per-cluster winner-take-all
+// with ties kept (Eq.(4)-(5) L220-225, readings R3/R4); per-probe convergence
+// and max_iters (Alg. 1); slot refill.
+//
+// At n_p = 4096 the A operand of a 128-probe tile (V^T as bytes) is 512 KiB,
+// so it cannot stay resident as in sos_tc2_kernel.  Instead it is streamed:
+// A-producer warps expand each K block of the state bits into a ring of
+// swizzled 16 KiB stages, once per pass, in step with the TMA ring of W tiles:
+//
+//   warp 0      TMA producer: W8 + gamma*I tiles (NP rows x 128 B per K block)
+//   warp 1      MMA issuer (one lane) and TMEM owner; two 256-column
+//               accumulators so the epilogue of pass p overlaps pass p+1
+//   warps 2-5   epilogue (thread = probe = TMEM lane): WTA of the pass's
+//               clusters, convergence, output, slot refill
+//   warps 6-9   A producers (thread = probe = A row): V bits -> A stage
+//
+// The current state V lives in shared memory ([word][probe], conflict-free);
+// the next state is written to a global scratch (L2) by the epilogue and
+// copied back into V at the end of the round (every A stage of the round has
+// been consumed by then: the last pass's accumulator is complete).
+#include <cuda.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "gb_internal.h"
+#include "gb_tc_common.cuh"
+
+namespace gb {
+namespace {
+using namespace tc;
+
+constexpr int kThreads3 = 320;
+
+struct Sos3Params {
+    int NP;          // columns per pass (whole clusters, <= 256)
+    int BR;          // TMA box rows
+    int S;           // W (B) stages
+    int SA;          // A stages
+    int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    uint32_t a_off, b_off, v_off, bar_off, b_stage;
+};
+
+template <int WC>
+__global__ void __launch_bounds__(kThreads3, 1)
+sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
+               const uint16_t *__restrict__ probes, int64_t k, int T, unsigned long long *queue,
+               uint32_t *__restrict__ vscratch, uint32_t *__restrict__ out_state,
+               uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status) {
+    constexpr int LP = 32 * WC;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    uint8_t *gbase = smem_raw + (base - raw);
+    const uint32_t A0 = base + P.a_off;     // SA x (128 x 128 B), SW128
+    const uint32_t B0 = base + P.b_off;     // S x (NP x 128 B), SW128
+    uint32_t *V = reinterpret_cast<uint32_t *>(gbase + P.v_off);   // [nw][128] current state
+    uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
+    const uint32_t bar0 = smem_u32(bars);
+    const int S = P.S, SA = P.SA;
+    auto full_bar = [&](int i) { return bar0 + 8u * i; };
+    auto empty_bar = [&](int i) { return bar0 + 8u * (S + i); };
+    auto afull_bar = [&](int i) { return bar0 + 8u * (2 * S + i); };
+    auto aempty_bar = [&](int i) { return bar0 + 8u * (2 * S + SA + i); };
+    auto tfull_bar = [&](int i) { return bar0 + 8u * (2 * S + 2 * SA + i); };
+    auto tempty_bar = [&](int i) { return bar0 + 8u * (2 * S + 2 * SA + 2 + i); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * S + 2 * SA + 4);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const bool epi = warp >= 2 && warp < 6;
+    const bool apro = warp >= 6;
+    const int m = 32 * (warp & 3) + lane;   // probe row = TMEM lane quarter of the warp (epilogue, A producers)
+    const int nw = s.nw, np = s.np;
+    const int nkb = (np + kKB - 1) / kKB;
+    const int npass = (np + P.NP - 1) / P.NP;
+    uint32_t *Vn = vscratch + (size_t)blockIdx.x * nw * kTM;   // next state [nw][128]
+
+    if (tid == 0) {
+        for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
+        for (int i = 0; i < SA; ++i) { mbar_init(afull_bar(i), 128); mbar_init(aempty_bar(i), 1); }
+        for (int i = 0; i < 2; ++i) { mbar_init(tfull_bar(i), 1); mbar_init(tempty_bar(i), 128); }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&wmap) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    uint32_t it_p = 0, it_m = 0, it_a = 0, pc_m = 0, pc_e = 0;
+    int64_t p = -1;
+    int rl = 0;
+    bool active = false;
+    auto refill = [&]() {
+        for (;;) {
+            p = (int64_t)atomicAdd(queue, 1ull);
+            for (int w = 0; w < nw; ++w) V[w * kTM + m] = 0u;
+            rl = 0;
+            if (p >= k) { active = false; return; }
+            bool valid = true;
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+            }
+            if (!valid) {   // GB_INVALID: zero state, 0 rounds; take another probe
+                uint32_t *out = out_state + p * nw;
+                for (int w = 0; w < nw; ++w) out[w] = 0u;
+                out_iters[p] = 0;
+                out_status[p] = GB_INVALID;
+                continue;
+            }
+            // ---- a1 ingest: V^0 known one-hot, erased 0
+            for (int c = 0; c < s.C; ++c) {
+                const unsigned sym = __ldg(probes + p * s.C + c);
+                if (sym != kErased) V[(c * WC + (int)(sym >> 5)) * kTM + m] = 1u << (sym & 31);
+            }
+            active = true;
+            return;
+        }
+    };
+    if (epi) refill();
+    for (;;) {
+        if (!__syncthreads_or(epi && active)) break;
+        if (warp == 0) {
+            if (lane == 0) {   // ---- TMA producer: W rows of each pass, K block by K block
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    for (int kb = 0; kb < nkb; ++kb, ++it_p) {
+                        const int st = it_p % S;
+                        mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
+                        mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);
+                        const uint32_t Bs = B0 + st * P.b_stage;
+                        for (int r0 = 0; r0 < ncols; r0 += P.BR)
+                            tma_load_2d(Bs + r0 * kKB, &wmap, full_bar(st), kb * kKB, n0 + r0);
+                    }
+                }
+            }
+            __syncwarp();
+        } else if (warp == 1) {
+            if (lane == 0) {   // ---- MMA issuer
+                for (int pass = 0; pass < npass; ++pass, ++pc_m) {
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    const uint32_t buf = pc_m & 1u;
+                    mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t idesc = i8_idesc(ncols);
+                    for (int kb = 0; kb < nkb; ++kb, ++it_m) {
+                        const int st = it_m % S, sa = it_m % SA;
+                        mbar_wait(afull_bar(sa), (it_m / SA) & 1u);
+                        mbar_wait(full_bar(st), (it_m / S) & 1u);
+                        tc_fence_after();
+                        const uint32_t As = A0 + sa * (kTM * kKB), Bs = B0 + st * P.b_stage;
+#pragma unroll
+                        for (int ks = 0; ks < kKB / 32; ++ks)
+                            umma_i8(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32), idesc,
+                                    (kb > 0 || ks > 0) ? 1u : 0u);
+                        umma_commit(empty_bar(st));
+                        umma_commit(aempty_bar(sa));
+                    }
+                    umma_commit(tfull_bar(buf));
+                }
+            }
+            __syncwarp();
+        } else if (apro) {
+            // ---- A producers: K block kb of A = probe m's state bits [128 kb, 128 kb + 128) as
+            // bytes, 128-byte swizzle (16-byte chunk ch of row m at ch ^ (m & 7)), once per pass
+            for (int pass = 0; pass < npass; ++pass) {
+                for (int kb = 0; kb < nkb; ++kb, ++it_a) {
+                    const int sa = it_a % SA;
+                    mbar_wait(aempty_bar(sa), ((it_a / SA) & 1u) ^ 1u);
+                    uint32_t wv[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) wv[q] = (4 * kb + q < nw) ? V[(4 * kb + q) * kTM + m] : 0u;
+                    uint8_t *arow = gbase + P.a_off + sa * (kTM * kKB) + m * kKB;
+#pragma unroll
+                    for (int ch = 0; ch < 8; ++ch) {
+                        const uint32_t bits = (wv[ch >> 1] >> ((ch & 1) * 16)) & 0xffffu;
+                        *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
+                            make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u), spread4((bits >> 8) & 15u),
+                                       spread4(bits >> 12));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_arrive(afull_bar(sa));
+                }
+            }
+        } else {
+            // ---- epilogue: per-cluster max + mask of each pass (a4)
+            bool changed = false;
+            const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+            for (int pass = 0; pass < npass; ++pass, ++pc_e) {
+                const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                const uint32_t buf = pc_e & 1u;
+                mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
+                tc_fence_after();
+                for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
+                    const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
+                    uint32_t mx = 0;
+                    for (int g = 0; g < WC; ++g) {
+                        uint32_t v32[32];
+                        tmem_ld32(tl + col + 32 * g, v32);
+                        const uint32_t vw = P.gamma_epi ? V[(c * WC + g) * kTM + m] : 0u;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                    }
+                    for (int g = 0; g < WC; ++g) {
+                        uint32_t v32[32];
+                        tmem_ld32(tl + col + 32 * g, v32);
+                        const uint32_t vw = V[(c * WC + g) * kTM + m];
+                        const uint32_t ve = P.gamma_epi ? vw : 0u;
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            word |= ((v32[j] + (((ve >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
+                        word &= real_mask(s.L, g);
+                        if (word != vw) changed = true;
+                        Vn[(c * WC + g) * kTM + m] = word;
+                    }
+                }
+                tc_fence_before();
+                mbar_arrive(tempty_bar(buf));
+            }
+            // ---- convergence (Alg. 1 "until V^{t+1} == V^t"), output, slot refill.  The
+            // last pass's accumulator is complete, so every A stage of this round has been
+            // consumed: V may be overwritten.
+            if (active) {
+                ++rl;
+                if (!changed || rl == T) {   // ---- a7 output
+                    uint32_t *out = out_state + p * nw;
+                    for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
+                    out_iters[p] = (uint16_t)rl;
+                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    refill();
+                } else {
+                    for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+template <int WC>
+cudaError_t launch3_t(gb_net *net, const Sos3Params &P, size_t smem, const CUtensorMap *map, const uint16_t *probes,
+                      int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    auto fn = sos_tc3_kernel<WC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+    const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    const size_t need = (size_t)net->sm_count * net->s.nw * kTM * sizeof(uint32_t);
+    if (net->vscratch_bytes < need) {
+        cudaFree(net->vscratch);
+        net->vscratch = nullptr;
+        net->vscratch_bytes = 0;
+        if (cudaMalloc(&net->vscratch, need) != cudaSuccess) {
+            cudaGetLastError();
+            return cudaErrorMemoryAllocation;
+        }
+        net->vscratch_bytes = need;
+    }
+    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, net->queue, net->vscratch, state,
+                                      iters, status);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
+    Sos3Params &P = *reinterpret_cast<Sos3Params *>(params);
+    if (s.Lp > 256 || s.np <= 1024 || s.np > 4096) return false;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4 && s.Wc != 8) return false;
+    P.NP = s.Lp * (256 / s.Lp);
+    if (P.NP > s.np) P.NP = s.np;
+    int br = 256;
+    while (br > 32 && s.Lp % br) br >>= 1;
+    P.BR = br;
+    P.gamma_epi = gamma > 255 ? gamma : 0;
+    P.b_stage = (uint32_t)P.NP * kKB;
+    const size_t vbytes = (size_t)s.nw * kTM * 4;
+    for (P.S = 4; P.S >= 2; --P.S) {
+        for (P.SA = 3; P.SA >= 2; --P.SA) {
+            P.a_off = 0;
+            P.b_off = (uint32_t)P.SA * kTM * kKB;
+            P.v_off = P.b_off + P.S * P.b_stage;
+            P.bar_off = (uint32_t)(P.v_off + vbytes);
+            smem = P.bar_off + 8 * (2 * P.S + 2 * P.SA + 4) + 16 + 1024;
+            if (smem <= 227 * 1024) return true;
+        }
+    }
+    return false;
+}
+
+static_assert(sizeof(Sos3Params) <= 64, "plan3 params buffer");
+int plan3_box_rows(const void *params) { return reinterpret_cast<const Sos3Params *>(params)->BR; }
+
+bool sos_tc3_enabled(const Shape &s) {
+    const char *env = getenv("GB_SOS_TC3");
+    if (env && env[0] == '0') return false;
+    Sos3Params P;
+    size_t smem;
+    return plan3(s, 1, &P, smem);
+}
+
+cudaError_t launch_sos_tc3(gb_net *net, int gamma, const void *map, const uint16_t *probes, int64_t k,
+                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    Sos3Params P;
+    size_t smem;
+    if (!plan3(net->s, gamma, &P, smem)) return cudaErrorNotSupported;
+    const CUtensorMap *m = reinterpret_cast<const CUtensorMap *>(map);
+    switch (net->s.Wc) {
+        case 1: return launch3_t<1>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+        case 2: return launch3_t<2>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+        case 4: return launch3_t<4>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+        default: return launch3_t<8>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+    }
+}
+
+}  // namespace gb

@@ -55,6 +55,9 @@ struct gb_net {
     alignas(64) unsigned char wmap_g[128];
     alignas(64) unsigned char wmap_g2[128];  // W8g map with the CTA-pair kernel's box (half the rows)
     bool wmap_g2_ok;
+    bool wmap_g_ok;                          // wmap_g encoded (sos_tc2 / pair kernels)
+    alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
+    bool wmap_g3_ok;
     int w8g_gamma;
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
     unsigned long long *queue;             // device work counter (slot-refill kernels)
@@ -92,6 +95,13 @@ cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, 
 bool decode_hyb8_supported(const Shape &s, int rule, int64_t k, const void *state);
 cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                                uint16_t *iters, uint8_t *status, cudaStream_t st);
+// Streamed-A sum-of-sum kernel for 1024 < n_p <= 4096 (gb_decode_sos_tc3.cu); the
+// caller has built W8g = W8 + gamma*I and its tensor map (box rows from plan3).
+bool plan3(const Shape &s, int gamma, void *params, size_t &smem);
+int plan3_box_rows(const void *params);
+bool sos_tc3_enabled(const Shape &s);
+cudaError_t launch_sos_tc3(gb_net *net, int gamma, const void *map, const uint16_t *probes, int64_t k,
+                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,

@@ -431,9 +431,9 @@ def test_determinism(gb):
             np.testing.assert_array_equal(x, y)
 
 
-@pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc2_kernel"), (16, 256, 0, "sos_tc_kernel"),
+@pytest.mark.parametrize("c,l,rule,want", [(8, 128, 0, "sos_tc2_kernel"), (16, 256, 0, "sos_tc3_kernel"),
                                            (4, 16, 0, "sos_tc2_kernel"), (3, 3, 0, "sos_tc2_kernel"),
-                                           (8, 256, 0, "sos_tc_kernel"), (4, 256, 0, "sos_tc2_kernel"),
+                                           (8, 256, 0, "sos_tc3_kernel"), (4, 256, 0, "sos_tc2_kernel"),
                                            (8, 128, 2, "decode_hyb8_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
@@ -525,3 +525,30 @@ def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
         np.testing.assert_array_equal(x, y)
     w8, _ = oracle.store(msgs, c, l)
     assert_same(res["1"], oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20), 0, "pair")
+
+
+@pytest.mark.parametrize("c,l,m,e,gamma,k", [(16, 256, 100000, 8, 2, 300), (32, 64, 3000, 16, 1, 700),
+                                             (9, 256, 20000, 4, 0, 257), (5, 250, 4000, 2, 300, 129),
+                                             (16, 256, 30000, 8, 255, 200)])
+def test_sos_streamed_a_vs_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
+    """The streamed-A SOS kernel (1024 < n_p <= 4096: A producer warps expand the
+    state into a ring of swizzled stages, TMA ring of W8 + gamma*I) equals the
+    oracle and the 4-warp sos_tc_kernel (GB_SOS_TC3=0) bit for bit: ragged tiles,
+    gamma = 0, gamma folded into B (<= 255) and added in the epilogue (300)."""
+    msgs = gbgen.messages(600 + c + l, m, c, l)
+    net = make_net(gb, msgs, c, l)
+    pr, _ = gbgen.probes(601 + c, msgs, k, e, l, random_count=k // 10)
+    pr[3, 0] = l                       # invalid symbol
+    monkeypatch.delenv("GB_SOS_TC3", raising=False)
+    assert net.decode_kernel(0) == "sos_tc3_kernel"
+    got = gpu_decode(net, pr, 0, gamma, 20)
+    w8, _ = oracle.store(msgs, c, l)
+    assert_same(got, oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20), 0, "tc3")
+    assert_same(gpu_decode(net, pr, 0, gamma, 3), oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=3),
+                0, "tc3 T=3")
+    monkeypatch.setenv("GB_SOS_TC3", "0")
+    assert net.decode_kernel(0) == "sos_tc_kernel"
+    other = gpu_decode(net, pr, 0, gamma, 20)
+    for x, y in zip(got, other):
+        np.testing.assert_array_equal(x, y)
+    net.close()

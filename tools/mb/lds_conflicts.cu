@@ -1,3 +1,13 @@
+// lds_conflicts.cu -- shared-memory wavefronts of 16-byte loads (LDS.128) by bank-group pattern.
+// Each lane reads 16 B from a random 128-B row at bank group g(lane) (the W bit-row layout of
+// decode_hyb8_kernel).  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o lds lds_conflicts.cu
+// Measured on B200 (ncu l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld / LDS instructions):
+//   pattern 0  g = lane & 7 (8 distinct groups per quarter-warp)   4.0 wavefronts (ideal)
+//   pattern 1  g = (lane >> 2) & 7                                 16.0
+//   pattern 2  g random                                              9.4  (= the decode kernel's 9.2)
+//   pattern 3  g = 0                                                32.0
+//   pattern 4  2 lanes per group in each quarter-warp                8.0
+// i.e. wavefronts are formed per quarter-warp (lanes 8q..8q+7) and a random row pick costs 2.3x.
 #include <cstdio>
 #include <cstdint>
 // each lane reads 16 B from row r (random) at bank group g(lane, pattern)
