@@ -26,6 +26,7 @@
 // copied back into V at the end of the round (every A stage of the round has
 // been consumed by then: the last pass's accumulator is complete).
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -297,8 +298,10 @@ bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
     P.gamma_epi = gamma > 255 ? gamma : 0;
     P.b_stage = (uint32_t)P.NP * kKB;
     const size_t vbytes = (size_t)s.nw * kTM * 4;
-    for (P.S = 4; P.S >= 2; --P.S) {
-        for (P.SA = 3; P.SA >= 2; --P.SA) {
+    int s_max = 4, sa_max = 3;
+    if (const char *env = getenv("GB_TC3_STAGES")) sscanf(env, "%d,%d", &s_max, &sa_max);   // experiments
+    for (P.S = s_max; P.S >= 2; --P.S) {
+        for (P.SA = sa_max; P.SA >= 2; --P.SA) {
             P.a_off = 0;
             P.b_off = (uint32_t)P.SA * kTM * kKB;
             P.v_off = P.b_off + P.S * P.b_stage;
