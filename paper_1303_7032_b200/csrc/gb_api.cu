@@ -347,7 +347,8 @@ const char *gb_decode_kernel(gb_net *net, int rule) {
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule == GB_HYBRID && gb::decode_hyb8_supported(net->s, rule, 0, nullptr)) return "decode_hyb8_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
-    if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule)) return "decode_l2_kernel";
+    if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule))
+        return gb::decode_l2t_supported(net->s, rule) ? "decode_l2t_kernel" : "decode_l2_kernel";
     return "decode_generic_kernel";
 }
 

@@ -37,7 +37,8 @@ template <int WC, int RULE>
 __global__ void __launch_bounds__(kL2Warps * 32)
 decode_l2_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k,
                  int T, uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
-                 uint8_t *__restrict__ out_status) {
+                 uint8_t *__restrict__ out_status, const int64_t *__restrict__ list,
+                 const unsigned long long *__restrict__ list_count) {
     constexpr int NG = 32 / WC;            // lane groups per warp
     constexpr int LP = 32 * WC;
     extern __shared__ uint32_t sm[];
@@ -47,7 +48,10 @@ decode_l2_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__res
     uint32_t *Xa = sm + warp * 2 * nw, *Xb = Xa + nw;
     const unsigned gmask = (WC == 32 ? 0xffffffffu : ((1u << WC) - 1u)) << (g * WC);
 
-    for (int64_t p = (int64_t)blockIdx.x * kL2Warps + warp; p < k; p += (int64_t)gridDim.x * kL2Warps) {
+    // list mode: decode only the probes queued by decode_l2t_kernel (more erased clusters than its slots)
+    const int64_t nprobe = list ? (int64_t)*list_count : k;
+    for (int64_t pi = (int64_t)blockIdx.x * kL2Warps + warp; pi < nprobe; pi += (int64_t)gridDim.x * kL2Warps) {
+        const int64_t p = list ? list[pi] : pi;
         const uint16_t *pr = probes + p * C;
         // ---- a1 ingest
         unsigned long long em = 0ull;
@@ -173,7 +177,8 @@ decode_l2_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__res
 
 template <int WC, int RULE>
 cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                     uint16_t *iters, uint8_t *status, cudaStream_t st) {
+                     uint16_t *iters, uint8_t *status, cudaStream_t st, const int64_t *list = nullptr,
+                     const unsigned long long *list_count = nullptr) {
     const size_t smem = (size_t)kL2Warps * 2 * net->s.nw * sizeof(uint32_t);
     auto fn = decode_l2_kernel<WC, RULE>;
     if (smem > 48 * 1024) {
@@ -182,8 +187,9 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
     }
     int64_t grid = (k + kL2Warps - 1) / kL2Warps;
     const int64_t cap = (int64_t)net->sm_count * 8;
-    if (grid > cap) grid = cap;
-    fn<<<(unsigned)grid, kL2Warps * 32, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status);
+    if (grid > cap || list) grid = cap;
+    fn<<<(unsigned)grid, kL2Warps * 32, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status,
+                                                    list, list_count);
     net->launches += 1;
     return cudaGetLastError();
 }
@@ -199,6 +205,34 @@ cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int
                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     if (!decode_l2_supported(net->s, rule)) return cudaErrorNotSupported;
     const bool h = rule == GB_HYBRID;
+    if (decode_l2t_supported(net->s, rule)) {
+        // thread-per-probe kernel; probes with more in-scope clusters than its slots are
+        // queued and decoded here by the warp-per-probe kernel in list mode
+        if (net->ovf_cap < k) {
+            cudaFree(net->ovf);
+            net->ovf = nullptr;
+            net->ovf_cap = 0;
+            if (cudaMalloc(&net->ovf, (size_t)k * sizeof(int64_t)) != cudaSuccess) {
+                cudaGetLastError();
+                return cudaErrorMemoryAllocation;
+            }
+            net->ovf_cap = k;
+        }
+        cudaError_t e = cudaMemsetAsync(net->ovf_count, 0, sizeof(unsigned long long), st);
+        if (e != cudaSuccess) return e;
+        e = launch_decode_l2t(net, probes, k, rule, max_iters, state, iters, status, st);
+        if (e != cudaSuccess) return e;
+        const int64_t *L = net->ovf;
+        const unsigned long long *LC = net->ovf_count;
+        switch (net->s.Wc) {
+            case 4: return h ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
+                             : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
+            case 8: return h ? launch_t<8, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
+                             : launch_t<8, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
+            default: return h ? launch_t<16, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
+                              : launch_t<16, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
+        }
+    }
     switch (net->s.Wc) {
         case 1: return h ? launch_t<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
                          : launch_t<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);

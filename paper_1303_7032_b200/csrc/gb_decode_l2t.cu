@@ -1,0 +1,281 @@
+// gb_decode_l2t.cu -- thread-per-probe SOM / hybrid decode for networks whose
+// bit rows do not fit in shared memory (C <= 16, Wc in {4, 8, 16}, e.g.
+// BASELINE C4 c=16 l=256: W bits = 2 MiB, L2-resident; Scenario 2 l=512).
+//
+// Same method and result as decode_l2_kernel (gb_decode_l2.cu), which keeps
+// the probes needing more slots than this kernel holds (list mode).  Here one
+// thread decodes one probe: its in-scope cluster states (erased clusters for
+// the hybrid, all clusters for sum-of-max) live in shared memory laid out
+// [slot word][thread] (conflict-free), old and next state in two areas
+// (synchronous rounds).  W bit-row blocks are read from L2 with 16-byte loads.
+//
+// Method:
+//  a1 ingest  -- symbols -> erased set; symbol >= L -> GB_INVALID.
+//  a5 prune   -- hybrid: X^0 on erased clusters = AND of the known neurons'
+//                rows (S^0 == C-e, Alg. 2 L2-5 / Thm 4); the known rows are
+//                walked once, each loading its blocks of every erased cluster.
+//                SOM: erased clusters all 1 (L270-271), known one-hot.
+//  a6 round   -- Eq.(6)-(7) by bail-out-early (Thm 1) in push form:
+//                for target t and source s != t, H = OR of block t of the rows
+//                of X_s, read in stages of up to 4 rows (the lowest remaining
+//                candidate of successive words, all in flight together) until
+//                H covers the still-alive part of X_t (L449); X'_t = X_t AND
+//                over s of H; an emptied target stops being walked (L450).
+//                Hybrid: known clusters frozen (Alg. 2).
+//  a7 output  -- state bits, rounds (incl. the confirming round), status.
+#include "gb_internal.h"
+
+namespace gb {
+namespace {
+
+constexpr int kMaxC16 = 16;
+
+template <int WC>
+__device__ __forceinline__ void ldg_block(const uint32_t *p, uint32_t (&v)[WC]) {
+    if constexpr (WC % 4 == 0) {
+#pragma unroll
+        for (int q = 0; q < WC / 4; ++q) {
+            const uint4 t = __ldg(reinterpret_cast<const uint4 *>(p) + q);
+            v[4 * q] = t.x; v[4 * q + 1] = t.y; v[4 * q + 2] = t.z; v[4 * q + 3] = t.w;
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < WC; ++u) v[u] = __ldg(p + u);
+    }
+}
+
+template <int WC, int RULE, int MAXS, int NT>
+__global__ void __launch_bounds__(NT, 1)
+decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int T,
+                  uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
+                  uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
+                  unsigned long long *__restrict__ ovf_count) {
+    constexpr int LP = 32 * WC;
+    extern __shared__ uint32_t sm[];
+    const int tid = threadIdx.x;
+    const int C = s.C, nw = s.nw;
+    uint32_t rmask[WC];
+#pragma unroll
+    for (int u = 0; u < WC; ++u) {
+        const int nb = min(32, max(0, s.L - u * 32));
+        rmask[u] = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    }
+    for (int64_t p = (int64_t)blockIdx.x * NT + tid; p < k; p += (int64_t)gridDim.x * NT) {
+        const uint16_t *pr = probes + p * C;
+        // ---- a1 ingest
+        uint32_t emask = 0u;
+        bool bad = false;
+        for (int c = 0; c < C; ++c) {
+            const unsigned sym = __ldg(pr + c);
+            if (sym == kErased) emask |= 1u << c;
+            else if (sym >= (unsigned)s.L) bad = true;
+        }
+        uint32_t *out = out_state + p * nw;
+        if (bad) {
+            for (int w = 0; w < nw; ++w) out[w] = 0u;
+            out_iters[p] = 0;
+            out_status[p] = GB_INVALID;
+            continue;
+        }
+        const uint32_t scope = (RULE == GB_SUM_OF_MAX) ? ((1u << C) - 1u) : emask;
+        const int nslot = __popc(scope);
+        if (nslot > MAXS) {   // more in-scope clusters than slots: warp-per-probe kernel (list mode)
+            ovf[atomicAdd(ovf_count, 1ull)] = p;
+            continue;
+        }
+        uint64_t slots = 0;   // in-scope clusters ascending, 4 bits each
+        {
+            uint32_t m = scope;
+#pragma unroll
+            for (int t = 0; t < MAXS; ++t) {
+                if (m) {
+                    slots |= (uint64_t)(__ffs(m) - 1) << (4 * t);
+                    m &= m - 1u;
+                }
+            }
+        }
+        auto slot_c = [&](int t) -> int { return (int)((slots >> (4 * t)) & 15u); };
+        uint32_t *X = sm, *Xn = sm + MAXS * WC * NT;
+        // ---- a5 prune (hybrid) / init (SOM)
+        if (RULE == GB_HYBRID) {
+            uint32_t x[MAXS][WC];
+#pragma unroll
+            for (int t = 0; t < MAXS; ++t)
+#pragma unroll
+                for (int u = 0; u < WC; ++u) x[t][u] = rmask[u];
+            uint32_t km = ((1u << C) - 1u) & ~emask;
+            while (km) {
+                const int kc = __ffs(km) - 1;
+                km &= km - 1u;
+                const uint32_t *row = wb + (size_t)(kc * LP + __ldg(pr + kc)) * nw;
+#pragma unroll
+                for (int t = 0; t < MAXS; ++t) {
+                    if (t < nslot) {
+                        uint32_t r[WC];
+                        ldg_block<WC>(row + slot_c(t) * WC, r);
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) x[t][u] &= r[u];
+                    }
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < MAXS; ++t)
+                if (t < nslot)
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) X[(t * WC + u) * NT + tid] = x[t][u];
+        } else {
+            for (int t = 0; t < nslot; ++t) {
+                const int c = slot_c(t);
+                if ((emask >> c) & 1u) {
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) X[(t * WC + u) * NT + tid] = rmask[u];
+                } else {
+                    const unsigned sym = __ldg(pr + c);
+#pragma unroll
+                    for (int u = 0; u < WC; ++u)
+                        X[(t * WC + u) * NT + tid] = ((int)(sym >> 5) == u) ? (1u << (sym & 31)) : 0u;
+                }
+            }
+        }
+        // ---- a6 synchronous rounds
+        int it = 0, status = GB_MAX_ITERS;
+        if (RULE == GB_HYBRID && nslot == 0) {
+            status = GB_CONVERGED;
+        } else {
+            while (it < T) {
+                bool changed = false;
+                for (int t = 0; t < nslot; ++t) {
+                    const int ct = slot_c(t);
+                    uint32_t alive[WC];
+                    uint32_t any = 0u;
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) {
+                        alive[u] = X[(t * WC + u) * NT + tid];
+                        any |= alive[u];
+                    }
+                    for (int si = 0; si < nslot && any; ++si) {
+                        if (si == t) continue;
+                        const uint32_t *base = wb + (size_t)(slot_c(si) * LP) * nw + ct * WC;
+                        uint32_t rem[WC];
+                        uint32_t left = 0u;
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) {
+                            rem[u] = X[(si * WC + u) * NT + tid];
+                            left |= rem[u];
+                        }
+                        uint32_t h[WC];
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) h[u] = 0u;
+                        uint32_t miss = 1u;
+                        while (miss && left) {
+                            // one stage: the lowest remaining candidate of successive words, <= 4 rows
+                            int cnt = 0;
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                if (rem[u] && cnt < 4) {
+                                    const uint32_t b = __ffs(rem[u]) - 1;
+                                    rem[u] &= rem[u] - 1u;
+                                    ++cnt;
+                                    uint32_t r[WC];
+                                    ldg_block<WC>(base + (size_t)(u * 32 + b) * nw, r);
+#pragma unroll
+                                    for (int v = 0; v < WC; ++v) h[v] |= r[v];
+                                }
+                            }
+                            miss = 0u;
+                            left = 0u;
+#pragma unroll
+                            for (int u = 0; u < WC; ++u) {
+                                miss |= alive[u] & ~h[u];
+                                left |= rem[u];
+                            }
+                        }
+                        any = 0u;
+#pragma unroll
+                        for (int u = 0; u < WC; ++u) {
+                            alive[u] &= h[u];
+                            any |= alive[u];
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < WC; ++u) {
+                        changed |= (alive[u] != X[(t * WC + u) * NT + tid]);
+                        Xn[(t * WC + u) * NT + tid] = alive[u];
+                    }
+                }
+                uint32_t *tmp = X; X = Xn; Xn = tmp;
+                ++it;
+                if (!changed) { status = GB_CONVERGED; break; }
+            }
+        }
+        // ---- a7 output: in-scope clusters from X, the others the known one-hot
+        for (int c = 0; c < C; ++c) {
+            uint32_t v[WC];
+            if ((scope >> c) & 1u) {
+                const int t = __popc(scope & ((1u << c) - 1u));
+#pragma unroll
+                for (int u = 0; u < WC; ++u) v[u] = X[(t * WC + u) * NT + tid];
+            } else {
+                const unsigned sym = __ldg(pr + c);
+#pragma unroll
+                for (int u = 0; u < WC; ++u) v[u] = ((int)(sym >> 5) == u) ? (1u << (sym & 31)) : 0u;
+            }
+            uint32_t *o = out + c * WC;
+            if constexpr (WC % 4 == 0) {
+#pragma unroll
+                for (int q = 0; q < WC / 4; ++q)
+                    reinterpret_cast<uint4 *>(o)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < WC; ++u) o[u] = v[u];
+            }
+        }
+        out_iters[p] = (uint16_t)it;
+        out_status[p] = (uint8_t)status;
+    }
+}
+
+template <int WC, int RULE, int MAXS>
+cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                     uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    constexpr int NT = (128 * 1024) / (MAXS * WC * 8) > 256 ? 256 : (128 * 1024) / (MAXS * WC * 8);
+    const size_t smem = (size_t)2 * MAXS * WC * NT * sizeof(uint32_t);
+    auto fn = decode_l2t_kernel<WC, RULE, MAXS, NT>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (k + NT - 1) / NT;
+    if (grid > net->sm_count) grid = net->sm_count;
+    fn<<<(unsigned)grid, NT, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status, net->ovf,
+                                         net->ovf_count);
+    net->launches += 1;
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool decode_l2t_supported(const Shape &s, int rule) {
+    if (getenv("GB_NO_L2T")) return false;
+    if (rule == GB_SUM_OF_MAX && getenv("GB_L2T_ALL")) return s.C <= kMaxC16 && (s.Wc == 4 || s.Wc == 8);
+    // measured (round 1): faster than the warp-per-probe kernel for the hybrid at Wc = 8 (C4:
+    // 4.2 vs 7.9 ms); slower for sum-of-max at C4 (6.4 vs 4.6 ms: 16 slots leave 4 warps per
+    // SM) and for Scenario 2's Wc = 16 (0.44 vs 0.35 ms), which keep decode_l2_kernel
+    if (rule != GB_HYBRID || s.C > kMaxC16) return false;
+    if (getenv("GB_L2T_ALL")) return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;   // experiments / tests
+    return s.Wc == 4 || s.Wc == 8;
+}
+
+cudaError_t launch_decode_l2t(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+    if (!decode_l2t_supported(net->s, rule)) return cudaErrorNotSupported;
+    const bool h = rule == GB_HYBRID;
+    switch (net->s.Wc) {
+        case 4: return h ? launch_t<4, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
+                         : launch_t<4, GB_SUM_OF_MAX, 16>(net, probes, k, max_iters, state, iters, status, st);
+        case 8: return h ? launch_t<8, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
+                         : launch_t<8, GB_SUM_OF_MAX, 16>(net, probes, k, max_iters, state, iters, status, st);
+        default: return h ? launch_t<16, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
+                          : cudaErrorNotSupported;
+    }
+}
+
+}  // namespace gb

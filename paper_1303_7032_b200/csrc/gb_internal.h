@@ -78,6 +78,11 @@ cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
 cudaError_t launch_or_bits(gb_net *net, const uint32_t *bits, int64_t count, cudaStream_t st);
 bool decode_smem_supported(const Shape &s, int rule);
 bool decode_l2_supported(const Shape &s, int rule);
+// thread-per-probe L2 kernel (gb_decode_l2t.cu): probes needing more slots than it
+// holds are appended to net->ovf (decode_l2_kernel decodes them in list mode).
+bool decode_l2t_supported(const Shape &s, int rule);
+cudaError_t launch_decode_l2t(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 bool sos_tc_supported(const Shape &s);

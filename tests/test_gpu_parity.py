@@ -436,10 +436,10 @@ def test_determinism(gb):
                                            (8, 256, 0, "sos_tc3_kernel"), (4, 256, 0, "sos_tc2_kernel"),
                                            (8, 128, 2, "decode_hyb8_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
-                                           (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2_kernel"),
+                                           (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2t_kernel"),
                                            (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2_kernel"),
                                            (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc_kernel"),
-                                           (16, 512, 2, "decode_l2_kernel"),
+                                           (16, 512, 2, "decode_l2_kernel"), (9, 100, 2, "decode_l2t_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
@@ -551,4 +551,36 @@ def test_sos_streamed_a_vs_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
     other = gpu_decode(net, pr, 0, gamma, 20)
     for x, y in zip(got, other):
         np.testing.assert_array_equal(x, y)
+    net.close()
+
+
+@pytest.mark.parametrize("c,l,m,e,k", [(16, 256, 100000, 8, 300), (16, 256, 20000, 11, 200), (12, 100, 3000, 5, 257),
+                                       (16, 512, 50000, 7, 100), (9, 128, 8000, 3, 129), (16, 200, 0, 6, 64)])
+@pytest.mark.parametrize("rule", [1, 2])
+def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule):
+    """The thread-per-probe L2 kernel (staged push from L2-resident bit rows) against
+    the oracle and against the warp-per-probe decode_l2_kernel (GB_NO_L2T): mixed
+    erasure counts (probes with more erased clusters than its 8 hybrid slots are
+    queued to the warp kernel), ragged L, M=0, invalid probes, random probes.
+    GB_L2T_ALL=1 also routes sum-of-max and Wc=16 through it (slower there, so not
+    the default, but it must stay exact)."""
+    monkeypatch.setenv("GB_L2T_ALL", "1")
+    msgs = gbgen.messages(700 + c + l + m, max(m, 1), c, l)[:m]
+    src = msgs if m else gbgen.messages(5, 10, c, l)
+    pr, _ = gbgen.probes(701 + k, src, k, e, l, random_count=k // 5)
+    rng = np.random.default_rng(k + c)
+    for i in range(0, k, 4):
+        row = pr[i].copy()
+        row[row == 0xFFFF] = rng.integers(0, l)
+        row[rng.choice(c, int(rng.integers(0, c + 1)), replace=False)] = 0xFFFF
+        pr[i] = row
+    pr[1, 0] = l
+    w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
+    net = make_net(gb, msgs, c, l)
+    want = oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=20)
+    assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, f"l2t c={c} l={l}")
+    assert_same(gpu_decode(net, pr, rule, 1, 2), oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=2), rule, "T=2")
+    monkeypatch.delenv("GB_L2T_ALL")
+    monkeypatch.setenv("GB_NO_L2T", "1")
+    assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, "warp kernel")
     net.close()
