@@ -30,7 +30,8 @@ import subprocess
 import numpy as np
 
 SOS, SOM, HYBRID = 0, 1, 2
-CONVERGED, MAX_ITERS, INVALID = 0, 1, 2
+CONVERGED, MAX_ITERS, INVALID, CYCLE = 0, 1, 2, 3
+CYCLE_EXIT = 1   # flag: stop an oscillating SOS probe at V^r == V^{r-2} (N4)
 ERASED = 0xFFFF
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -59,6 +60,8 @@ def _load():
         lib.oracle_store.restype = i64
         lib.oracle_decode.argtypes = [P, i32, i32, P, i64, i32, i32, i32, P, P, P, P]
         lib.oracle_decode.restype = i32
+        lib.oracle_decode_flags.argtypes = [P, i32, i32, P, i64, i32, i32, i32, i32, P, P, P, P]
+        lib.oracle_decode_flags.restype = i32
         lib.oracle_sos_trace.argtypes = [P, i32, i32, P, i32, i32, P, P]
         lib.oracle_sos_trace.restype = i32
         lib.oracle_som_step.argtypes = [P, i32, i32, P, i32, P]
@@ -89,7 +92,7 @@ def store(msgs: np.ndarray, c: int, l: int, w: np.ndarray | None = None):
 
 
 def decode(w: np.ndarray, c: int, l: int, probes: np.ndarray, rule: int,
-           gamma: int = 2, max_iters: int = 20, with_blocks: bool = False):
+           gamma: int = 2, max_iters: int = 20, with_blocks: bool = False, flags: int = 0):
     """Decode probes (uint16 [K, C], 0xFFFF = erased) under ``rule``.
 
     Returns (state uint32 [K, C*Wc], iters uint16 [K], status uint8 [K]
@@ -104,9 +107,9 @@ def decode(w: np.ndarray, c: int, l: int, probes: np.ndarray, rule: int,
     iters = np.zeros(k, dtype=np.uint16)
     status = np.zeros(k, dtype=np.uint8)
     blocks = np.zeros(k, dtype=np.int64) if with_blocks else None
-    rc = _load().oracle_decode(_ptr(w), c, l, _ptr(probes), k, rule, gamma, max_iters,
-                               _ptr(state), _ptr(iters), _ptr(status),
-                               _ptr(blocks) if with_blocks else None)
+    rc = _load().oracle_decode_flags(_ptr(w), c, l, _ptr(probes), k, rule, gamma, max_iters, flags,
+                                     _ptr(state), _ptr(iters), _ptr(status),
+                                     _ptr(blocks) if with_blocks else None)
     if rc != 0:
         raise ValueError("oracle_decode: invalid arguments")
     if with_blocks:

@@ -22,6 +22,10 @@
  * count is the number of rounds executed including the round that shows no
  * change; status CONVERGED when V^r == V^{r-1} for some r <= T, else
  * MAX_ITERS with V^T returned.  Hybrid counts only its bail-out rounds.
+ * Optional (flag OR_CYCLE_EXIT, SOS only, SPEC S:L304 design
+ * decision): a round r >= 2 whose state repeats the state of round r-2
+ * (V^r == V^{r-2} != V^{r-1}, the period-2 oscillation PAPER.md L515-517
+ * exhibits) stops the probe with status CYCLE and V^r returned.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -29,7 +33,8 @@
 
 #define OR_ERASED 0xFFFFu
 enum { OR_SOS = 0, OR_SOM = 1, OR_HYBRID = 2 };
-enum { OR_CONVERGED = 0, OR_MAX_ITERS = 1, OR_INVALID = 2 };
+enum { OR_CONVERGED = 0, OR_MAX_ITERS = 1, OR_INVALID = 2, OR_CYCLE = 3 };
+enum { OR_CYCLE_EXIT = 1 };
 
 /* ------------------------------------------------------------------ */
 /* STORE  ("we add edges to the network connecting all
@@ -149,14 +154,14 @@ static int64_t bailout_blocks(const uint8_t *W, int C, int L, const uint8_t *V,
 }
 
 typedef struct {
-    uint8_t *V, *Vn;
+    uint8_t *V, *Vn, *V2;
     int64_t *S;
     uint8_t *scope;
 } scratch_t;
 
 /* Decode one probe.  Returns status; writes rounds to *iters. */
 static int decode_one(const uint8_t *W, int C, int L, const uint16_t *p,
-                      int rule, int gamma, int T, scratch_t *sc,
+                      int rule, int gamma, int T, int flags, scratch_t *sc,
                       uint16_t *iters, int64_t *blocks)
 {
     const int64_t n = (int64_t)C * L;
@@ -183,9 +188,13 @@ static int decode_one(const uint8_t *W, int C, int L, const uint16_t *p,
         for (int r = 1; r <= T; ++r) {
             sos_round(W, C, L, gamma, V, Vn, sc->S);
             int conv = same(V, Vn, n);
+            /* V2 holds V^{r-2} (valid for r >= 2) */
+            int cyc = (flags & OR_CYCLE_EXIT) && r >= 2 && same(Vn, sc->V2, n);
+            memcpy(sc->V2, V, (size_t)n);
             memcpy(V, Vn, (size_t)n);
             work += 1;
             if (conv) { *iters = (uint16_t)r; if (blocks) *blocks = work; return OR_CONVERGED; }
+            if (cyc) { *iters = (uint16_t)r; if (blocks) *blocks = work; return OR_CYCLE; }
         }
         *iters = (uint16_t)T;
         if (blocks) *blocks = work;
@@ -263,10 +272,24 @@ static int decode_one(const uint8_t *W, int C, int L, const uint16_t *p,
  * out_iters uint16 [K]; out_status uint8 [K]; out_blocks int64 [K] or NULL.
  * Returns 0, or -1 on bad arguments (rule, gamma, T).  OpenMP over probes
  * (independent columns of Eq.(11)).                   */
+int oracle_decode_flags(const uint8_t *W, int C, int L, const uint16_t *probes,
+                        int64_t K, int rule, int gamma, int T, int flags,
+                        uint32_t *out_state, uint16_t *out_iters,
+                        uint8_t *out_status, int64_t *out_blocks);
+
 int oracle_decode(const uint8_t *W, int C, int L, const uint16_t *probes,
                   int64_t K, int rule, int gamma, int T,
                   uint32_t *out_state, uint16_t *out_iters,
                   uint8_t *out_status, int64_t *out_blocks)
+{
+    return oracle_decode_flags(W, C, L, probes, K, rule, gamma, T, 0, out_state,
+                               out_iters, out_status, out_blocks);
+}
+
+int oracle_decode_flags(const uint8_t *W, int C, int L, const uint16_t *probes,
+                        int64_t K, int rule, int gamma, int T, int flags,
+                        uint32_t *out_state, uint16_t *out_iters,
+                        uint8_t *out_status, int64_t *out_blocks)
 {
     if (C < 2 || L < 1 || T < 1 || T > 65535 || gamma < 0) return -1;
     if (rule != OR_SOS && rule != OR_SOM && rule != OR_HYBRID) return -1;
@@ -278,20 +301,21 @@ int oracle_decode(const uint8_t *W, int C, int L, const uint16_t *probes,
         scratch_t sc;
         sc.V = (uint8_t *)malloc((size_t)n);
         sc.Vn = (uint8_t *)malloc((size_t)n);
+        sc.V2 = (uint8_t *)malloc((size_t)n);
         sc.S = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
         sc.scope = (uint8_t *)malloc((size_t)C);
 #pragma omp for schedule(dynamic, 16)
         for (int64_t k = 0; k < K; ++k) {
             uint16_t it = 0;
             int64_t blk = 0;
-            int st = decode_one(W, C, L, probes + k * C, rule, gamma, T, &sc,
+            int st = decode_one(W, C, L, probes + k * C, rule, gamma, T, flags, &sc,
                                 &it, out_blocks ? &blk : NULL);
             pack_state(sc.V, C, L, out_state + k * nw);
             out_iters[k] = it;
             out_status[k] = (uint8_t)st;
             if (out_blocks) out_blocks[k] = blk;
         }
-        free(sc.V); free(sc.Vn); free(sc.S); free(sc.scope);
+        free(sc.V); free(sc.Vn); free(sc.V2); free(sc.S); free(sc.scope);
     }
     return 0;
 }

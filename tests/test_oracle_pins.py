@@ -143,6 +143,57 @@ def test_sos_oscillation_decode_never_converges(T):
     np.testing.assert_array_equal(oracle.unpack_state(st, 3, 3)[0], want)
 
 
+@pytest.mark.parametrize("T", [3, 4, 20])
+def test_sos_cycle_exit_paper_l515(T):
+    """N4 cycle exit (flag-gated): on the printed oscillation of
+    PAPER.md L515-517 (gamma=1, v^3 == v^1 != v^2) the probe stops at round 3
+    with status CYCLE and state v^3 = v^1 (printed); with T < 3 the cap wins;
+    gamma=2 (L525) still converges in 3 rounds; SOM/hybrid are unaffected."""
+    msgs, _, t = va_network()
+    w, _ = oracle.store(msgs, 3, 3)
+    probe = np.array([[ERASED, ERASED, 0]], dtype=np.uint16)
+    st, it, ss = oracle.decode(w, 3, 3, probe, SOS, gamma=1, max_iters=T, flags=oracle.CYCLE_EXIT)
+    assert ss[0] == oracle.CYCLE and it[0] == 3
+    np.testing.assert_array_equal(oracle.unpack_state(st, 3, 3)[0], t["v3"])
+    np.testing.assert_array_equal(oracle.unpack_state(st, 3, 3)[0], t["v1"])
+    st, it, ss = oracle.decode(w, 3, 3, probe, SOS, gamma=1, max_iters=2, flags=oracle.CYCLE_EXIT)
+    assert ss[0] == MAX_ITERS and it[0] == 2
+    np.testing.assert_array_equal(oracle.unpack_state(st, 3, 3)[0], t["v2"])
+    st, it, ss = oracle.decode(w, 3, 3, probe, SOS, gamma=2, max_iters=T, flags=oracle.CYCLE_EXIT)
+    assert ss[0] == CONVERGED and it[0] == 3
+    for rule in (SOM, HYBRID):
+        a = oracle.decode(w, 3, 3, probe, rule, gamma=1, max_iters=T, flags=oracle.CYCLE_EXIT)
+        b = oracle.decode(w, 3, 3, probe, rule, gamma=1, max_iters=T)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+
+
+def test_sos_cycle_exit_is_the_literal_run_stopped_early():
+    """The cycle-exit result of every probe equals the literal (flag-free) run
+    cut at the exit round: same state at T = exit round, and a literal run of
+    exit+2j rounds returns the same state (period 2)."""
+    rng_seed = 11
+    c, l = 5, 6
+    msgs, w = rand_instance(rng_seed, c, l, 25)
+    pr, _ = gbgen.probes(rng_seed + 1, msgs, 300, 3, l, random_count=100)
+    st, it, ss = oracle.decode(w, c, l, pr, SOS, gamma=0, max_iters=20, flags=oracle.CYCLE_EXIT)
+    cyc = np.flatnonzero(ss == oracle.CYCLE)
+    assert cyc.size > 0   # gamma=0 oscillates often on this instance
+    for i in cyc[:40]:
+        r = int(it[i])
+        for T in (r, r + 2, r + 4):
+            s2, i2, q2 = oracle.decode(w, c, l, pr[i:i + 1], SOS, gamma=0, max_iters=T)
+            assert q2[0] == MAX_ITERS and i2[0] == T
+            np.testing.assert_array_equal(s2[0], st[i])
+        s3, _, _ = oracle.decode(w, c, l, pr[i:i + 1], SOS, gamma=0, max_iters=r - 1)
+        assert not np.array_equal(s3[0], st[i])
+    rest = np.flatnonzero(ss != oracle.CYCLE)
+    s4, i4, q4 = oracle.decode(w, c, l, pr[rest], SOS, gamma=0, max_iters=20)
+    np.testing.assert_array_equal(s4, st[rest])
+    np.testing.assert_array_equal(i4, it[rest])
+    np.testing.assert_array_equal(q4, ss[rest])
+
+
 def test_sos_gamma2_converges_paper_l525():
     """PAPER.md L525 "If we increase gamma = 2, then the network converges".
     Hand-derived: v^1 = (1,1,1,1,1,1,1,0,0), s^1 = (5,4,4,4,5,4,8,0,0),
