@@ -61,8 +61,23 @@ enum {
 enum {
     GB_CONVERGED = 0,      /* V^r == V^{r-1} for some round r <= max_iters     */
     GB_MAX_ITERS = 1,      /* max_iters rounds ran without a fixed point        */
-    GB_INVALID = 2         /* a probe symbol was >= L (and not GB_ERASED); the
+    GB_INVALID = 2,        /* a probe symbol was >= L (and not GB_ERASED); the
                               state is all zero and iters is 0                  */
+    GB_CYCLE = 3           /* only with GB_FLAG_CYCLE_EXIT: sum-of-sum state of
+                              round r repeats round r-2 (period-2 oscillation)  */
+};
+
+/* gb_decode_ex flags. */
+enum {
+    GB_FLAG_CYCLE_EXIT = 1 /* sum-of-sum: stop a probe at the first round r >= 2
+                              with V^r == V^{r-2} != V^{r-1} (the period-2
+                              oscillation of PAPER.md L515-522) with status
+                              GB_CYCLE, iters r and state V^r, instead of running
+                              to max_iters.  SURVEY.md §8.f N4 / SPEC S:L304.
+                              Changes the returned state (V^r, not V^max_iters),
+                              so it is off by default.  No effect on sum-of-max
+                              and hybrid, whose rounds only remove neurons
+                              (Lemma 1) and cannot oscillate.                     */
 };
 
 #define GB_ERASED 0xFFFFu
@@ -177,6 +192,14 @@ int gb_seal(gb_net *net, void *stream);
 int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
               int max_iters, uint32_t *out_state, uint16_t *out_iters,
               uint8_t *out_status, void *stream);
+
+/*
+ * gb_decode_ex -- gb_decode with option flags (GB_FLAG_*); flags == 0 is
+ * gb_decode.  Unknown flag bits -> GB_EINVAL.
+ */
+int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
+                 int max_iters, unsigned flags, uint32_t *out_state, uint16_t *out_iters,
+                 uint8_t *out_status, void *stream);
 
 /* gb_info -- shape and bookkeeping; any out pointer may be NULL.
  * stored_count counts messages passed to gb_store since create/clear.      */

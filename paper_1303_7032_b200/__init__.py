@@ -20,7 +20,8 @@ import numpy as np
 
 SUM_OF_SUM, SUM_OF_MAX, HYBRID = 0, 1, 2
 SOS, SOM = SUM_OF_SUM, SUM_OF_MAX
-CONVERGED, MAX_ITERS, INVALID = 0, 1, 2
+CONVERGED, MAX_ITERS, INVALID, CYCLE = 0, 1, 2, 3
+FLAG_CYCLE_EXIT = 1   # gb_decode_ex: stop an oscillating sum-of-sum probe at V^r == V^{r-2}
 ERASED = 0xFFFF
 GB_OK, GB_EINVAL, GB_ENOMEM, GB_ECUDA, GB_ESTATE, GB_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 
@@ -29,7 +30,7 @@ LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB:
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_bits", "gb_or_bits", "gb_seal",
-           "gb_decode", "gb_info", "gb_launch_count", "gb_decode_kernel", "gb_last_error",
+           "gb_decode", "gb_decode_ex", "gb_info", "gb_launch_count", "gb_decode_kernel", "gb_last_error",
            "gb_version")
 
 _lib = None
@@ -61,6 +62,7 @@ def lib() -> ctypes.CDLL:
         "gb_bits": ([P, PP, ctypes.POINTER(i64)], i32),
         "gb_or_bits": ([P, P, i64, P], i32),
         "gb_decode": ([P, P, i64, i32, i32, i32, P, P, P, P], i32),
+        "gb_decode_ex": ([P, P, i64, i32, i32, i32, ctypes.c_uint, P, P, P, P], i32),
         "gb_info": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                      ctypes.POINTER(i64)], i32),
         "gb_launch_count": ([P, ctypes.POINTER(i64)], i32),
@@ -190,7 +192,7 @@ class Net:
         return state, iters, status
 
     def decode(self, probes, rule: int, gamma: int = 2, max_iters: int = 20, out=None,
-               stream=None):
+               stream=None, flags: int = 0):
         """gb_decode.  ``probes``: uint16-bit [K, C] torch tensor (cuda or host)
         or numpy array.  Returns (state int32 [K, nw], iters int16 [K],
         status uint8 [K]) on the probes' side (bit patterns; view as unsigned)."""
@@ -203,7 +205,7 @@ class Net:
             else:
                 out = self.alloc_outputs(k, device=probes.is_cuda)
         state, iters, status = out
-        _check(lib().gb_decode(self._h, ctypes.c_void_p(_addr(probes)), k, rule, gamma, max_iters,
-                               ctypes.c_void_p(_addr(state)), ctypes.c_void_p(_addr(iters)),
-                               ctypes.c_void_p(_addr(status)), _stream(stream)))
+        _check(lib().gb_decode_ex(self._h, ctypes.c_void_p(_addr(probes)), k, rule, gamma, max_iters, flags,
+                                  ctypes.c_void_p(_addr(state)), ctypes.c_void_p(_addr(iters)),
+                                  ctypes.c_void_p(_addr(status)), _stream(stream)))
         return state, iters, status

@@ -15,7 +15,7 @@ namespace gb {
 cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
                                uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k, int rule,
-                                  int gamma, int max_iters, uint32_t *state, uint16_t *iters,
+                                  int gamma, int max_iters, int cyc, uint32_t *state, uint16_t *iters,
                                   uint8_t *status, cudaStream_t st);
 }
 
@@ -266,7 +266,14 @@ int gb_seal(gb_net *net, void *stream) {
 
 int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
               uint32_t *out_state, uint16_t *out_iters, uint8_t *out_status, void *stream) {
+    return gb_decode_ex(net, probes, k, rule, gamma, max_iters, 0u, out_state, out_iters, out_status, stream);
+}
+
+int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
+                 unsigned flags, uint32_t *out_state, uint16_t *out_iters, uint8_t *out_status, void *stream) {
     if (!net) return fail(GB_EINVAL, "gb_decode: net is NULL");
+    if (flags & ~(unsigned)GB_FLAG_CYCLE_EXIT) return fail(GB_EINVAL, "gb_decode: unknown flags 0x%x", flags);
+    const int cyc = (rule == GB_SUM_OF_SUM && (flags & GB_FLAG_CYCLE_EXIT)) ? 1 : 0;
     if (rule != GB_SUM_OF_SUM && rule != GB_SUM_OF_MAX && rule != GB_HYBRID)
         return fail(GB_EINVAL, "gb_decode: unknown rule %d", rule);
     if (gamma < 0 || gamma > 65535) return fail(GB_EINVAL, "gb_decode: gamma %d outside [0, 65535]", gamma);
@@ -286,7 +293,7 @@ int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamm
     if (l0 < 0 || l1 < 0 || l2 < 0 || l3 < 0)
         return fail(GB_EINVAL, "gb_decode: buffer on another device");
     if (l0 && l1 && l2 && l3) {
-        GB_CUDA(gb::launch_decode(net, probes, k, rule, gamma, max_iters, out_state, out_iters,
+        GB_CUDA(gb::launch_decode(net, probes, k, rule, gamma, max_iters, cyc, out_state, out_iters,
                                   out_status, st),
                 "gb_decode: launch");
         return GB_OK;
@@ -318,7 +325,7 @@ int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamm
         uint8_t *dt = (uint8_t *)(di + chunk);
         GB_CUDA(cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, ss),
                 "gb_decode: H2D");
-        GB_CUDA(gb::launch_decode(net, dp, n, rule, gamma, max_iters, ds, di, dt, ss), "gb_decode: launch");
+        GB_CUDA(gb::launch_decode(net, dp, n, rule, gamma, max_iters, cyc, ds, di, dt, ss), "gb_decode: launch");
         GB_CUDA(cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
                                 cudaMemcpyDeviceToHost, ss), "gb_decode: D2H state");
         GB_CUDA(cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, ss),
@@ -364,18 +371,18 @@ namespace gb {
 
 // Kernel selection for one decode call.
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
-                          int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
+                          int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st) {
     cudaError_t e = cudaErrorNotSupported;
     if (rule == GB_SUM_OF_SUM) {
         if (sos_tc2_supported(net->s) || sos_tc3_enabled(net->s) || (net->wmap_ok && sos_tc_supported(net->s)))
-            e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, state, iters, status, st);
+            e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
     } else {
         e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
         if (e == cudaErrorNotSupported) e = launch_decode_l2(net, probes, k, rule, max_iters, state, iters, status, st);
     }
     if (e != cudaErrorNotSupported) return e;
-    return launch_decode_generic(net, probes, k, rule, gamma, max_iters, state, iters, status, st);
+    return launch_decode_generic(net, probes, k, rule, gamma, max_iters, cyc, state, iters, status, st);
 }
 
 }  // namespace gb

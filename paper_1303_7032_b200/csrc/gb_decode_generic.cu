@@ -37,7 +37,7 @@ __device__ __forceinline__ unsigned real_mask(const Shape &s, int u) {
 
 __global__ void __launch_bounds__(kWarps * 32)
 decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes,
-                      int64_t k, int rule, int gamma, int T, uint32_t *__restrict__ out_state,
+                      int64_t k, int rule, int gamma, int T, int cyc_exit, uint32_t *__restrict__ out_state,
                       uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status) {
     extern __shared__ uint32_t smem[];
     const int warp = threadIdx.x >> 5;
@@ -102,6 +102,7 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
             it = 0;
         } else {
             while (it < T) {
+                bool cyc = cyc_exit && it >= 1;   // Xn holds V^{r-2} from round r = it + 1 >= 2 on
                 if (rule == GB_SUM_OF_SUM) {
                     // pass 1: per-word max of the scores of real neurons
                     for (int w = lane; w < nw; w += 32) {
@@ -134,6 +135,7 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
                             for (int v = 0; v < nw; ++v) sc += __popc(__ldg(row + v) & X[v]);
                             if (sc == cm) nx |= 1u << b;
                         }
+                        cyc &= (Xn[w] == nx);
                         Xn[w] = nx;
                     }
                 } else {
@@ -166,9 +168,11 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
                 bool diff = false;
                 for (int w = lane; w < nw; w += 32) diff |= (Xn[w] != X[w]);
                 diff = __any_sync(0xffffffffu, diff);
+                cyc = __all_sync(0xffffffffu, cyc) && rule == GB_SUM_OF_SUM;
                 uint32_t *tmp = X; X = Xn; Xn = tmp;
                 ++it;
                 if (!diff) { status = GB_CONVERGED; break; }
+                if (cyc) { status = GB_CYCLE; break; }   // V^r == V^{r-2} (GB_FLAG_CYCLE_EXIT)
             }
         }
         for (int w = lane; w < nw; w += 32) out[w] = X[w];
@@ -183,7 +187,7 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
 }  // namespace
 
 cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k, int rule,
-                                  int gamma, int max_iters, uint32_t *state, uint16_t *iters,
+                                  int gamma, int max_iters, int cyc, uint32_t *state, uint16_t *iters,
                                   uint8_t *status, cudaStream_t st) {
     const size_t smem = (size_t)kWarps * 3 * net->s.nw * sizeof(uint32_t);
     int64_t grid = (k + kWarps - 1) / kWarps;
@@ -195,7 +199,7 @@ cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k
         if (e != cudaSuccess) return e;
     }
     decode_generic_kernel<<<(unsigned)grid, kWarps * 32, smem, st>>>(
-        net->s, net->wb, probes, k, rule, gamma, max_iters, state, iters, status);
+        net->s, net->wb, probes, k, rule, gamma, max_iters, cyc, state, iters, status);
     net->launches += 1;
     return cudaGetLastError();
 }

@@ -39,6 +39,7 @@ struct Pair2Params {
     int BR;          // TMA box rows (divides NP/2 for every pass)
     int S;           // B stages
     int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    int cyc;         // GB_FLAG_CYCLE_EXIT: stop a probe when V^r == V^{r-2}
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
@@ -235,6 +236,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         V = Vs + par * nw * kTM;
         Vn = Vs + (par ^ 1u) * nw * kTM;
         bool changed = false;
+        bool cyc = true;
         if (epi) {   // incremental A = V^T (bytes, SW128), as in sos_tc2_kernel
             uint32_t d = dirty;
             while (d) {
@@ -331,6 +333,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != old) { changed = true; dirty |= wbit; }
                             if (old) nzcur |= wbit;
+                            if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     } else {
@@ -356,6 +359,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != vw) { changed = true; dirty |= wbit; }
                             if (vw) nzcur |= wbit;
+                            if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     }
@@ -365,11 +369,12 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             }
             if (active) {   // convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
                 ++rl;
-                if (!changed || rl == T) {   // ---- a7 output
+                const bool cyc_stop = P.cyc && rl >= 2 && cyc && changed;   // V^r == V^{r-2}
+                if (!changed || rl == T || cyc_stop) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
                     for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
-                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    out_status[p] = (uint8_t)(!changed ? GB_CONVERGED : cyc_stop ? GB_CYCLE : GB_MAX_ITERS);
                     dirty |= nzcur;
                     refill();
                 } else {
@@ -398,6 +403,7 @@ bool plan_pair(const Shape &s, int gamma_epi, Pair2Params &P, size_t &smem) {
     while (br > 8 && (s.Lp / 2) % br) br >>= 1;
     P.BR = br;
     P.gamma_epi = gamma_epi;
+    P.cyc = 0;
     const int nkb = (s.np + kKB - 1) / kKB;
     P.a_off = 0;
     P.b_off = (uint32_t)nkb * kTM * kKB;
@@ -466,11 +472,12 @@ int sos_2cta_box_rows(const Shape &s) {
     return plan_pair(s, 0, P, smem) ? P.BR : 0;
 }
 
-cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, int64_t k, int max_iters,
+cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, int cyc, const uint16_t *probes, int64_t k, int max_iters,
                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     Pair2Params P;
     size_t smem;
     if (!plan_pair(net->s, gamma_epi, P, smem)) return cudaErrorNotSupported;
+    P.cyc = cyc;
     // one CTA per SM: two 512-column TMEM allocations on one SM could deadlock across pairs
     if (smem < 120 * 1024) smem = 120 * 1024;
     switch (net->s.Wc) {

@@ -47,7 +47,8 @@ struct SosParams {
 template <int WC>
 __global__ void __launch_bounds__(kThreads, 1)
 sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
-              const uint16_t *__restrict__ probes, int64_t k, int gamma, int T, unsigned long long *queue,
+              const uint16_t *__restrict__ probes, int64_t k, int gamma, int T, int cyc_exit,
+              unsigned long long *queue,
               uint32_t *vscratch,
               uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
               uint8_t *__restrict__ out_status) {
@@ -94,10 +95,13 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
     // Slot refill (as in sos_tc2_kernel): each TMEM lane holds one probe; a probe
     // that converges or reaches max_iters is written out and replaced by the
     // next probe of the global queue.
+    // per-thread double buffer: V = V^{r-1} (current), Vn receives V^r and holds V^{r-2} until
+    // then (the period-2 check of GB_FLAG_CYCLE_EXIT reads it before overwriting)
     uint32_t *V = Vs, *Vn = Vs + nw * kTM;
     int64_t p = -1;
     int rl = 0;
     bool active = false;
+    bool cyc = false;
     auto refill = [&]() {
         for (;;) {
             p = (int64_t)atomicAdd(queue, 1ull);
@@ -203,7 +207,9 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
                             uint32_t word = 0;
 #pragma unroll
                             for (int j = 0; j < 32; ++j) word |= (sc[32 * g + j] == mx ? 1u : 0u) << j;
-                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            word &= real_mask(s.L, g);
+                            if (cyc_exit) cyc &= (Vn[(c * WC + g) * kTM + m] == word);
+                            Vn[(c * WC + g) * kTM + m] = word;
                         }
                     } else {
                         uint32_t mx = 0;
@@ -223,7 +229,9 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
 #pragma unroll
                             for (int j = 0; j < 32; ++j)
                                 word |= ((v32[j] + (((vw >> j) & 1u) ? (uint32_t)gamma : 0u)) == mx ? 1u : 0u) << j;
-                            Vn[(c * WC + g) * kTM + m] = word & real_mask(s.L, g);
+                            word &= real_mask(s.L, g);
+                            if (cyc_exit) cyc &= (Vn[(c * WC + g) * kTM + m] == word);
+                            Vn[(c * WC + g) * kTM + m] = word;
                         }
                     }
                 }
@@ -235,15 +243,17 @@ sos_tc_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, SosParams P,
                 ++rl;
                 bool changed = false;
                 for (int w = 0; w < nw; ++w) changed |= (Vn[w * kTM + m] != V[w * kTM + m]);
-                for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
-                if (!changed || rl == T) {   // ---- a7 output
+                const bool cyc_stop = cyc_exit && rl >= 2 && cyc && changed;   // V^r == V^{r-2}
+                uint32_t *t = V; V = Vn; Vn = t;                             // V^r is current
+                if (!changed || rl == T || cyc_stop) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
                     for (int w = 0; w < nw; ++w) out[w] = V[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
-                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    out_status[p] = (uint8_t)(!changed ? GB_CONVERGED : cyc_stop ? GB_CYCLE : GB_MAX_ITERS);
                     refill();
                 }
             }
+            cyc = true;
             __syncthreads();
         }
         __syncthreads();
@@ -266,6 +276,7 @@ struct Sos2Params {
     int BR;          // TMA box rows
     int S;           // B stages
     int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    int cyc;         // GB_FLAG_CYCLE_EXIT: stop a probe when V^r == V^{r-2}
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
@@ -399,6 +410,7 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
         V = Vs + par * nw * kTM;
         Vn = Vs + (par ^ 1u) * nw * kTM;
         bool changed = false;
+        bool cyc = true;
         if (epi) {
             // A = V^T as bytes (128 x 128 B swizzled tile per K block), kept resident and
             // updated incrementally: only the state words that differ from what A holds
@@ -500,6 +512,7 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != old) { changed = true; dirty |= wbit; }
                             if (old) nzcur |= wbit;
+                            if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     } else {
@@ -524,6 +537,7 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
                             const uint32_t wbit = 1u << (c * WC + g);
                             if (word != vw) { changed = true; dirty |= wbit; }
                             if (vw) nzcur |= wbit;
+                            if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
                             Vn[(c * WC + g) * kTM + m] = word;
                         }
                     }
@@ -534,11 +548,12 @@ sos_tc2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos2Params P,
             // ---- convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
             if (active) {
                 ++rl;
-                if (!changed || rl == T) {   // ---- a7 output
+                const bool cyc_stop = P.cyc && rl >= 2 && cyc && changed;   // V^r == V^{r-2}
+                if (!changed || rl == T || cyc_stop) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
                     for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
-                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    out_status[p] = (uint8_t)(!changed ? GB_CONVERGED : cyc_stop ? GB_CYCLE : GB_MAX_ITERS);
                     // A still holds the expansion of the probe's state before this round
                     // (V); the new probe's V^0 goes into the same buffer
                     dirty |= nzcur;
@@ -563,6 +578,7 @@ bool plan2(const Shape &s, int gamma, Sos2Params &P, size_t &smem) {
     while (br > 32 && s.Lp % br) br >>= 1;
     P.BR = br;
     P.gamma_epi = gamma > 255 ? gamma : 0;
+    P.cyc = 0;
     const int nkb = (s.np + kKB - 1) / kKB;
     P.a_off = 0;
     P.b_off = (uint32_t)nkb * kTM * kKB;
@@ -617,7 +633,7 @@ bool plan(const Shape &s, SosParams &P, size_t &smem) {
 }
 
 template <int WC>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters, int cyc,
                      uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     SosParams P;
     size_t smem;
@@ -647,7 +663,7 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, 
     e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     fn<<<grid, kThreads, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap), P, probes, k,
-                                     gamma, max_iters, net->queue, net->vscratch, state, iters, status);
+                                     gamma, max_iters, cyc, net->queue, net->vscratch, state, iters, status);
     net->launches += 1;
     return cudaGetLastError();
 }
@@ -767,7 +783,7 @@ static cudaError_t ensure_w8g(gb_net *net, int gamma, cudaStream_t st) {
 }
 
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
-                                 uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     Sos2Params P2;
     size_t smem2;
     if (sos_tc3_enabled(net->s)) {   // 1024 < n_p <= 4096: streamed A tile
@@ -780,10 +796,11 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
             net->wmap_g3_ok = sos_encode_map(net, net->w8g, plan3_box_rows(pb), net->wmap_g3);
             if (!net->wmap_g3_ok) return cudaErrorNotSupported;
         }
-        return launch_sos_tc3(net, gamma, net->wmap_g3, probes, k, max_iters, state, iters, status, st);
+        return launch_sos_tc3(net, gamma, cyc, net->wmap_g3, probes, k, max_iters, state, iters, status, st);
     }
     if (plan2(net->s, gamma, P2, smem2) &&
         (net->s.Wc == 1 || net->s.Wc == 2 || net->s.Wc == 3 || net->s.Wc == 4 || net->s.Wc == 8)) {
+        P2.cyc = cyc;
         const bool fresh = !net->w8g;
         cudaError_t e = ensure_w8g(net, gamma, st);
         if (e != cudaSuccess) return e;
@@ -796,7 +813,7 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
                 net->wmap_g2_ok = sos_encode_map(net, net->w8g, sos_2cta_box_rows(net->s), net->wmap_g2);
                 if (!net->wmap_g2_ok) return cudaErrorNotSupported;
             }
-            return launch_sos_2cta(net, gamma > 255 ? gamma : 0, probes, k, max_iters, state, iters, status, st);
+            return launch_sos_2cta(net, gamma > 255 ? gamma : 0, cyc, probes, k, max_iters, state, iters, status, st);
         }
         if (smem2 < 120 * 1024) smem2 = 120 * 1024;   // one CTA per SM (512 TMEM columns)
         switch (net->s.Wc) {
@@ -808,12 +825,12 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
         }
     }
     switch (net->s.Wc) {
-        case 1: return launch_t<1>(net, probes, k, gamma, max_iters, state, iters, status, st);
-        case 2: return launch_t<2>(net, probes, k, gamma, max_iters, state, iters, status, st);
-        case 3: return launch_t<3>(net, probes, k, gamma, max_iters, state, iters, status, st);
-        case 4: return launch_t<4>(net, probes, k, gamma, max_iters, state, iters, status, st);
-        case 8: return launch_t<8>(net, probes, k, gamma, max_iters, state, iters, status, st);
-        case 16: return launch_t<16>(net, probes, k, gamma, max_iters, state, iters, status, st);
+        case 1: return launch_t<1>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 2: return launch_t<2>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 3: return launch_t<3>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 4: return launch_t<4>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 8: return launch_t<8>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 16: return launch_t<16>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
         default: return cudaErrorNotSupported;
     }
 }

@@ -47,6 +47,7 @@ struct Sos3Params {
     int S;           // W (B) stages
     int SA;          // A stages
     int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
+    int cyc;         // GB_FLAG_CYCLE_EXIT: stop a probe when V^r == V^{r-2}
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
@@ -83,7 +84,9 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
     const int nw = s.nw, np = s.np;
     const int nkb = (np + kKB - 1) / kKB;
     const int npass = (np + P.NP - 1) / P.NP;
-    uint32_t *Vn = vscratch + (size_t)blockIdx.x * nw * kTM;   // next state [nw][128]
+    // next state [nw][128] in a global scratch, two areas: round r writes area r & 1, which
+    // holds V^{r-2} until then (V^0 is put in area 0 at refill when the cycle exit is on)
+    uint32_t *Vn2 = vscratch + (size_t)blockIdx.x * 2 * nw * kTM;
 
     if (tid == 0) {
         for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
@@ -129,6 +132,8 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
                 const unsigned sym = __ldg(probes + p * s.C + c);
                 if (sym != kErased) V[(c * WC + (int)(sym >> 5)) * kTM + m] = 1u << (sym & 31);
             }
+            if (P.cyc)
+                for (int w = 0; w < nw; ++w) Vn2[w * kTM + m] = V[w * kTM + m];
             active = true;
             return;
         }
@@ -200,7 +205,8 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
             }
         } else {
             // ---- epilogue: per-cluster max + mask of each pass (a4)
-            bool changed = false;
+            bool changed = false, cyc = true;
+            uint32_t *Vn = Vn2 + (size_t)((rl + 1) & 1) * nw * kTM;   // area of round r = rl + 1
             const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
                 const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
@@ -229,6 +235,7 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
                             word |= ((v32[j] + (((ve >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
                         word &= real_mask(s.L, g);
                         if (word != vw) changed = true;
+                        if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
                         Vn[(c * WC + g) * kTM + m] = word;
                     }
                 }
@@ -240,11 +247,12 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
             // consumed: V may be overwritten.
             if (active) {
                 ++rl;
-                if (!changed || rl == T) {   // ---- a7 output
+                const bool cyc_stop = P.cyc && rl >= 2 && cyc && changed;   // V^r == V^{r-2}
+                if (!changed || rl == T || cyc_stop) {   // ---- a7 output
                     uint32_t *out = out_state + p * nw;
                     for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
                     out_iters[p] = (uint16_t)rl;
-                    out_status[p] = (uint8_t)(changed ? GB_MAX_ITERS : GB_CONVERGED);
+                    out_status[p] = (uint8_t)(!changed ? GB_CONVERGED : cyc_stop ? GB_CYCLE : GB_MAX_ITERS);
                     refill();
                 } else {
                     for (int w = 0; w < nw; ++w) V[w * kTM + m] = Vn[w * kTM + m];
@@ -265,7 +273,7 @@ cudaError_t launch3_t(gb_net *net, const Sos3Params &P, size_t smem, const CUten
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
-    const size_t need = (size_t)net->sm_count * net->s.nw * kTM * sizeof(uint32_t);
+    const size_t need = (size_t)net->sm_count * 2 * net->s.nw * kTM * sizeof(uint32_t);
     if (net->vscratch_bytes < need) {
         cudaFree(net->vscratch);
         net->vscratch = nullptr;
@@ -296,6 +304,7 @@ bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
     while (br > 32 && s.Lp % br) br >>= 1;
     P.BR = br;
     P.gamma_epi = gamma > 255 ? gamma : 0;
+    P.cyc = 0;
     P.b_stage = (uint32_t)P.NP * kKB;
     const size_t vbytes = (size_t)s.nw * kTM * 4;
     int s_max = 4, sa_max = 3;
@@ -324,11 +333,12 @@ bool sos_tc3_enabled(const Shape &s) {
     return plan3(s, 1, &P, smem);
 }
 
-cudaError_t launch_sos_tc3(gb_net *net, int gamma, const void *map, const uint16_t *probes, int64_t k,
+cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     Sos3Params P;
     size_t smem;
     if (!plan3(net->s, gamma, &P, smem)) return cudaErrorNotSupported;
+    P.cyc = cyc;
     const CUtensorMap *m = reinterpret_cast<const CUtensorMap *>(map);
     switch (net->s.Wc) {
         case 1: return launch3_t<1>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);

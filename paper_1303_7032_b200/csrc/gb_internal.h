@@ -93,7 +93,7 @@ bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out);
 // has built W8g = W8 + gamma*I (gamma_epi = gamma when gamma > 255, else 0).
 bool sos_2cta_enabled(const Shape &s);
 int sos_2cta_box_rows(const Shape &s);
-cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, const uint16_t *probes, int64_t k, int max_iters,
+cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, int cyc, const uint16_t *probes, int64_t k, int max_iters,
                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 // C = 8, Wc = 4 hybrid decode of the probes with e <= 4 (gb_decode_hyb8.cu); the
 // others are appended to net->ovf.
@@ -105,12 +105,13 @@ cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, i
 bool plan3(const Shape &s, int gamma, void *params, size_t &smem);
 int plan3_box_rows(const void *params);
 bool sos_tc3_enabled(const Shape &s);
-cudaError_t launch_sos_tc3(gb_net *net, int gamma, const void *map, const uint16_t *probes, int64_t k,
+cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+// cyc = 1: period-2 cycle exit (GB_FLAG_CYCLE_EXIT) in every sum-of-sum kernel
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
-                                 uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
-                          int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
+                          int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status,
                           cudaStream_t st);
 
 }  // namespace gb

@@ -584,3 +584,50 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule
     monkeypatch.setenv("GB_NO_L2T", "1")
     assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, "warp kernel")
     net.close()
+
+
+@pytest.mark.parametrize("c,l,m,e,k,gamma,env,kernel", [
+    (3, 3, 4, 2, 1, 1, {}, "sos_tc2x2_kernel"),                        # §V-A: v^3 == v^1
+    (5, 6, 25, 3, 300, 0, {}, "sos_tc2x2_kernel"),
+    (5, 6, 25, 3, 300, 0, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
+    (8, 128, 30000, 5, 1000, 1, {}, "sos_tc2x2_kernel"),
+    (8, 128, 20000, 4, 1000, 2, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
+    (16, 256, 100000, 10, 300, 0, {}, "sos_tc3_kernel"),
+    (16, 256, 100000, 10, 300, 0, {"GB_SOS_TC3": "0"}, "sos_tc_kernel"),
+    (8, 512, 30000, 5, 200, 0, {}, "sos_tc_kernel"),
+    (4, 600, 3000, 2, 100, 0, {}, "decode_generic_kernel"),
+])
+def test_sos_cycle_exit_flag(gb, monkeypatch, c, l, m, e, k, gamma, env, kernel):
+    """GB_FLAG_CYCLE_EXIT: every sum-of-sum kernel stops a probe at
+    the first round r >= 2 with V^r == V^{r-2} != V^{r-1}, status GB_CYCLE, state
+    V^r -- bit-exact vs the oracle with the same flag; without the flag nothing
+    changes; the flag leaves sum-of-max / hybrid untouched."""
+    for kk, v in env.items():
+        monkeypatch.setenv(kk, v)
+    if m == 4:
+        msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
+        pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
+    else:
+        msgs = gbgen.messages(800 + c + l, m, c, l)
+        pr, _ = gbgen.probes(801 + c, msgs, k, e, l, random_count=k // 3)
+    w, _ = oracle.store(msgs, c, l)
+    net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(0) == kernel
+    for T in (20, 7):
+        want = oracle.decode(w, c, l, pr, 0, gamma=gamma, max_iters=T, flags=oracle.CYCLE_EXIT)
+        st, it, ss = net.decode(to_dev(pr), 0, gamma=gamma, max_iters=T, flags=gb.FLAG_CYCLE_EXIT)
+        torch.cuda.synchronize()
+        got = (st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy())
+        assert_same(got, want, 0, f"cycle-exit {kernel} T={T}")
+        if m == 4:
+            assert want[2][0] == gb.CYCLE and want[1][0] == 3
+    assert (want[2] == gb.CYCLE).any()
+    assert_same(gpu_decode(net, pr, 0, gamma, 20), oracle.decode(w, c, l, pr, 0, gamma=gamma, max_iters=20), 0)
+    for rule in (1, 2):
+        st, it, ss = net.decode(to_dev(pr), rule, gamma=1, max_iters=20, flags=gb.FLAG_CYCLE_EXIT)
+        torch.cuda.synchronize()
+        got = (st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy())
+        assert_same(got, oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=20), rule, "flag on SOM/hybrid")
+    with pytest.raises(gb.GBError):
+        net.decode(to_dev(pr), 0, gamma=gamma, max_iters=20, flags=2)
+    net.close()
