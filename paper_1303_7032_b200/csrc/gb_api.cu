@@ -352,6 +352,7 @@ const char *gb_decode_kernel(gb_net *net, int rule) {
         return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net->s)) return "sos_tc3_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
+    if (rule == GB_SUM_OF_MAX && gb::som_tc_enabled(net->s)) return "som_tc_kernel";
     if (rule == GB_HYBRID && gb::decode_hyb8_supported(net->s, rule, 0, nullptr)) return "decode_hyb8_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule))
@@ -378,7 +379,9 @@ cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int ru
         if (sos_tc2_supported(net->s) || sos_tc3_enabled(net->s) || (net->wmap_ok && sos_tc_supported(net->s)))
             e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
     } else {
-        e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
+        if (rule == GB_SUM_OF_MAX && som_tc_enabled(net->s))
+            e = launch_som_tc(net, probes, k, max_iters, state, iters, status, st);
+        if (e == cudaErrorNotSupported) e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
         if (e == cudaErrorNotSupported) e = launch_decode_l2(net, probes, k, rule, max_iters, state, iters, status, st);
     }
     if (e != cudaErrorNotSupported) return e;

@@ -58,6 +58,8 @@ struct gb_net {
     bool wmap_g_ok;                          // wmap_g encoded (sos_tc2 / pair kernels)
     alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
     bool wmap_g3_ok;
+    alignas(64) unsigned char wmap_som[128]; // W8 map for the tensor-core sum-of-max kernel
+    bool wmap_som_ok;
     int w8g_gamma;
     unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
     unsigned long long *queue;             // device work counter (slot-refill kernels)
@@ -108,6 +110,10 @@ bool sos_tc3_enabled(const Shape &s);
 cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 // cyc = 1: period-2 cycle exit (GB_FLAG_CYCLE_EXIT) in every sum-of-sum kernel
+// exact sum-of-max on the tensor cores (gb_decode_som_tc.cu, N2), opt-in with GB_SOM_TC=1
+bool som_tc_enabled(const Shape &s);
+cudaError_t launch_som_tc(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                          uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,

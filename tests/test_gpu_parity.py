@@ -631,3 +631,30 @@ def test_sos_cycle_exit_flag(gb, monkeypatch, c, l, m, e, k, gamma, env, kernel)
     with pytest.raises(gb.GBError):
         net.decode(to_dev(pr), 0, gamma=gamma, max_iters=20, flags=2)
     net.close()
+
+
+@pytest.mark.parametrize("c,l,m,e,k", [(8, 128, 5000, 4, 1000), (8, 128, 20000, 4, 700), (4, 16, 50, 2, 1000),
+                                       (3, 3, 4, 2, 1), (5, 60, 2000, 3, 300), (16, 64, 3000, 9, 257),
+                                       (7, 100, 0, 3, 64)])
+def test_som_tensor_core_matches_oracle(gb, monkeypatch, c, l, m, e, k):
+    """N2: sum-of-max as C exact per-source-cluster int8 contractions on the tensor
+    cores (hit = count > 0, Eq.(6)-(7)) equals the oracle and the bit kernel bit for
+    bit: states, rounds, statuses; ragged L, C=16, M=0, the §V-A example, T=2."""
+    monkeypatch.setenv("GB_SOM_TC", "1")
+    if m == 4:
+        msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
+        pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
+    else:
+        msgs = gbgen.messages(900 + c + l, max(m, 1), c, l)[:m]
+        pr, _ = gbgen.probes(901 + c, msgs if m else gbgen.messages(4, 10, c, l), k, e, l, random_count=k // 5)
+        pr[2, 0] = l
+    w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
+    net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(1) == "som_tc_kernel"
+    for T in (20, 2):
+        want = oracle.decode(w, c, l, pr, 1, gamma=1, max_iters=T)
+        assert_same(gpu_decode(net, pr, 1, 1, T), want, 1, f"som_tc T={T}")
+    monkeypatch.delenv("GB_SOM_TC")
+    assert net.decode_kernel(1) != "som_tc_kernel"
+    assert_same(gpu_decode(net, pr, 1, 3, 20), oracle.decode(w, c, l, pr, 1, gamma=3, max_iters=20), 1, "bit")
+    net.close()

@@ -15,7 +15,7 @@ NCU="timeout 300 ncu --set full --clock-control none --import-source on"
 $NCU -k regex:decode_hyb8 -s 2 -c 1 -o gpurun_out/prof_hyb_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 $NCU -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 > /dev/null 2>&1
 $NCU -k regex:sos_tc -s 1 -c 1 -o gpurun_out/prof_sosc4_$TAG python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --config c4 --rule 0 --probes 20000 > /dev/null 2>&1
-$NCU -k regex:decode_l2 -s 1 -c 1 -o gpurun_out/prof_l2_$TAG python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --config c4 --rule 2 --probes 1000000 > /dev/null 2>&1
+$NCU -k regex:decode_l2t -s 1 -c 1 -o gpurun_out/prof_l2_$TAG python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu --config c4 --rule 2 --probes 1000000 > /dev/null 2>&1
 $NCU -k regex:store_priv -s 2 -c 1 -o gpurun_out/prof_store_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c5 > /dev/null 2>&1
 rm -f gpurun_out/bench_rules_$TAG.jsonl
 for a in "--config c2 --rule 0" "--config c2 --rule 1" "--config c2 --rule 2" "--config c2 --rule 0 --probes 1000000" "--config c2 --rule 2 --probes 10000000" "--config c4 --rule 0 --probes 100000" "--config c4 --rule 1 --probes 100000" "--config c4 --rule 2" "--config c1 --rule 2" "--config s2 --rule 2" "--config s2 --rule 0" "--config c5"; do

@@ -1,4 +1,10 @@
-"""Small decode/store workload for compute-sanitizer (memcheck / racecheck / synccheck)."""
+"""Small decode/store workload for compute-sanitizer (memcheck / racecheck / synccheck).
+
+Covers every kernel family: store (scattered + privatised) + apply + seal, OR of packed
+partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l2 (list mode),
+SOS pair / streamed-A / 4-warp / generic, the cycle-exit flag, and the tensor-core SOM kernel.
+"""
+import os
 import sys
 import numpy as np
 import torch
@@ -6,14 +12,33 @@ sys.path.insert(0, ".")
 import gbgen
 import paper_1303_7032_b200 as gb
 
-for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 500, 100, 5), (3, 3, 4, 20, 2)):
+for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 500, 100, 5), (3, 3, 4, 20, 2),
+                        (16, 256, 20000, 150, 8), (12, 100, 3000, 100, 5), (8, 512, 3000, 64, 4),
+                        (4, 600, 300, 50, 2)):
     msgs = gbgen.messages(1, m, c, l)
     pr, _ = gbgen.probes(2, msgs, k, e, l, random_count=k // 10)
+    rng = np.random.default_rng(k)
+    for i in range(0, k, 5):   # mixed erasure counts (wide-slot / list-mode paths)
+        pr[i, rng.choice(c, int(rng.integers(0, c + 1)), replace=False)] = 0xFFFF
     net = gb.Net(c, l)
     net.store(torch.from_numpy(msgs.view(np.int16)).cuda())
     net.seal()
+    probes = torch.from_numpy(pr.view(np.int16)).cuda()
     for rule in (0, 1, 2):
-        net.decode(torch.from_numpy(pr.view(np.int16)).cuda(), rule, gamma=2, max_iters=6)
+        net.decode(probes, rule, gamma=2, max_iters=6)
+    net.decode(probes, 0, gamma=0, max_iters=6, flags=gb.FLAG_CYCLE_EXIT)
+    if c == 8 and l == 128:
+        os.environ["GB_SOM_TC"] = "1"
+        net.decode(probes, 1, gamma=1, max_iters=6)
+        del os.environ["GB_SOM_TC"]
+        part = gb.Net(c, l)
+        part.store(torch.from_numpy(msgs[: m // 2].view(np.int16)).cuda())
+        part.seal()
+        fresh = gb.Net(c, l)
+        fresh.or_bits(torch.stack([part.bits(), net.bits()]).contiguous())
+        fresh.seal()
+        part.close()
+        fresh.close()
     torch.cuda.synchronize()
     net.close()
 print("sanitize workload done")
