@@ -350,7 +350,8 @@ const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
         return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
-    if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net->s)) return "sos_tc3_kernel";
+    if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net->s))
+        return gb::sos_tc3_pair(net->s) ? "sos_tc3x2_kernel" : "sos_tc3_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule == GB_SUM_OF_MAX && gb::som_tc_enabled(net->s)) return "som_tc_kernel";
     if (rule == GB_HYBRID && gb::decode_hyb8_supported(net->s, rule, 0, nullptr)) return "decode_hyb8_kernel";

@@ -43,57 +43,6 @@ struct Pair2Params {
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
-__device__ __forceinline__ uint32_t cta_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(rank));
-    return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ void st_cluster_u32(uint32_t a, uint32_t v) {
-    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
-}
-// Arrive on a barrier of either CTA of the pair (address from mapa).  Default
-// .release.cta semantics: the epilogue only has to order its (waited)
-// tcgen05.ld's before the arrive, which tcgen05.fence::before_thread_sync does;
-// .release.cluster would add a GPU-scope fence behind the output stores.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t a) {
-    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
-}
-// TMA into this CTA's shared memory, transaction bytes counted on the leader's barrier.
-__device__ __forceinline__ void tma_load_2d_pair(uint32_t dst, const CUtensorMap *map, uint32_t bar_leader, int x,
-                                                 int y) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"((uint64_t)map), "r"(bar_leader), "r"(x), "r"(y) : "memory");
-}
-// Instruction descriptor: kind::i8, D = s32, A = B = u8, K-major, M = 256 (pair), N.
-__device__ __forceinline__ uint32_t i8_idesc_pair(int n) {
-    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
-}
-__device__ __forceinline__ void umma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accum) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
-}
-// Arrive on the barrier at the same offset in both CTAs once the pair's MMAs complete.
-__device__ __forceinline__ void umma_commit_pair(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-            bar),
-        "h"((uint16_t)3) : "memory");
-}
-
 template <int WC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params P,

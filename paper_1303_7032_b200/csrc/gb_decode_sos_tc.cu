@@ -789,11 +789,13 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
     if (sos_tc3_enabled(net->s)) {   // 1024 < n_p <= 4096: streamed A tile
         cudaError_t e = ensure_w8g(net, gamma, st);
         if (e != cudaSuccess) return e;
-        if (!net->wmap_g3_ok) {
-            alignas(8) unsigned char pb[64];
-            size_t smem3;
-            if (!plan3(net->s, gamma, pb, smem3)) return cudaErrorNotSupported;
-            net->wmap_g3_ok = sos_encode_map(net, net->w8g, plan3_box_rows(pb), net->wmap_g3);
+        alignas(8) unsigned char pb[64];
+        size_t smem3;
+        if (!plan3(net->s, gamma, pb, smem3)) return cudaErrorNotSupported;
+        const int br = plan3_box_rows(pb);   // differs between the pair and the 1-CTA form
+        if (!net->wmap_g3_ok || net->wmap_g3_br != br) {
+            net->wmap_g3_ok = sos_encode_map(net, net->w8g, br, net->wmap_g3);
+            net->wmap_g3_br = br;
             if (!net->wmap_g3_ok) return cudaErrorNotSupported;
         }
         return launch_sos_tc3(net, gamma, cyc, net->wmap_g3, probes, k, max_iters, state, iters, status, st);

@@ -58,6 +58,7 @@ struct gb_net {
     bool wmap_g_ok;                          // wmap_g encoded (sos_tc2 / pair kernels)
     alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
     bool wmap_g3_ok;
+    int wmap_g3_br;                          // box rows wmap_g3 was encoded with
     alignas(64) unsigned char wmap_som[128]; // W8 map for the tensor-core sum-of-max kernel
     bool wmap_som_ok;
     int w8g_gamma;
@@ -107,6 +108,7 @@ cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, i
 bool plan3(const Shape &s, int gamma, void *params, size_t &smem);
 int plan3_box_rows(const void *params);
 bool sos_tc3_enabled(const Shape &s);
+bool sos_tc3_pair(const Shape &s);   // the streamed-A kernel runs on CTA pairs
 cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 // cyc = 1: period-2 cycle exit (GB_FLAG_CYCLE_EXIT) in every sum-of-sum kernel

@@ -445,8 +445,8 @@ def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
     (tensor-core SOS, shared-memory bit kernel, generic warp kernel).  SOS at
     n_padded <= 1024 runs on a CTA pair (sos_tc2x2_kernel) unless GB_SOS_2CTA=0."""
-    if want == "sos_tc2_kernel" and os.environ.get("GB_SOS_2CTA", "1") != "0":
-        want = "sos_tc2x2_kernel"
+    if want in ("sos_tc2_kernel", "sos_tc3_kernel") and os.environ.get("GB_SOS_2CTA", "1") != "0":
+        want = want.replace("_kernel", "x2_kernel")
     net = gb.Net(c, l)
     assert net.decode_kernel(rule) == want
 
@@ -540,12 +540,15 @@ def test_sos_streamed_a_vs_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
     pr, _ = gbgen.probes(601 + c, msgs, k, e, l, random_count=k // 10)
     pr[3, 0] = l                       # invalid symbol
     monkeypatch.delenv("GB_SOS_TC3", raising=False)
-    assert net.decode_kernel(0) == "sos_tc3_kernel"
-    got = gpu_decode(net, pr, 0, gamma, 20)
     w8, _ = oracle.store(msgs, c, l)
-    assert_same(got, oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20), 0, "tc3")
-    assert_same(gpu_decode(net, pr, 0, gamma, 3), oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=3),
-                0, "tc3 T=3")
+    want = oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20)
+    for flag, name in (("1", "sos_tc3x2_kernel"), ("0", "sos_tc3_kernel")):   # CTA pair / single CTA
+        monkeypatch.setenv("GB_SOS_2CTA", flag)
+        assert net.decode_kernel(0) == name
+        got = gpu_decode(net, pr, 0, gamma, 20)
+        assert_same(got, want, 0, name)
+        assert_same(gpu_decode(net, pr, 0, gamma, 3),
+                    oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=3), 0, name + " T=3")
     monkeypatch.setenv("GB_SOS_TC3", "0")
     assert net.decode_kernel(0) == "sos_tc_kernel"
     other = gpu_decode(net, pr, 0, gamma, 20)
@@ -592,7 +595,8 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule
     (5, 6, 25, 3, 300, 0, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
     (8, 128, 30000, 5, 1000, 1, {}, "sos_tc2x2_kernel"),
     (8, 128, 20000, 4, 1000, 2, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
-    (16, 256, 100000, 10, 300, 0, {}, "sos_tc3_kernel"),
+    (16, 256, 100000, 10, 300, 0, {}, "sos_tc3x2_kernel"),
+    (16, 256, 100000, 10, 300, 0, {"GB_SOS_2CTA": "0"}, "sos_tc3_kernel"),
     (16, 256, 100000, 10, 300, 0, {"GB_SOS_TC3": "0"}, "sos_tc_kernel"),
     (8, 512, 30000, 5, 200, 0, {}, "sos_tc_kernel"),
     (4, 600, 3000, 2, 100, 0, {}, "decode_generic_kernel"),
