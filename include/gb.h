@@ -24,7 +24,10 @@
  *    back in host memory.  Device-pointer calls are asynchronous and
  *    stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
  *  - The caller owns all input/output buffers.  The library owns W (u8 and
- *    bit-packed) and its scratch.
+ *    bit-packed) and its scratch.  The scratch (work queues, overflow lists,
+ *    state buffers) is per handle, so calls on one handle must be
+ *    stream-ordered: issue them on one stream (or order the streams with
+ *    events); use one handle per stream for concurrent decodes.
  *  - Errors: functions return GB_OK (0) or a negative GB_E* code and set a
  *    thread-local message readable with gb_last_error().  No exception or
  *    abort crosses the ABI.  There is no CPU fallback: without a usable

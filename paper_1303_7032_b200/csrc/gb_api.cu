@@ -162,6 +162,7 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->ovf);
     cudaFree(net->ovf_count);
     cudaFree(net->spart);
+    cudaFree(net->xscratch);
     free(net);
     return GB_OK;
 }

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(NT, 1)
 decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int T,
                   uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
                   uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
-                  unsigned long long *__restrict__ ovf_count) {
+                  unsigned long long *__restrict__ ovf_count, uint32_t *__restrict__ xscratch) {
     constexpr int LP = 32 * WC;
     extern __shared__ uint32_t sm[];
     const int tid = threadIdx.x;
@@ -95,7 +95,10 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
             }
         }
         auto slot_c = [&](int t) -> int { return (int)((slots >> (4 * t)) & 15u); };
-        uint32_t *X = sm, *Xn = sm + MAXS * WC * NT;
+        // current state in shared memory, next state in this CTA's slice of a global scratch
+        // ([word][thread], L2): only the current state is read in the push loops, so shared
+        // memory holds one copy and twice as many threads fit (latency hiding of the L2 rows)
+        uint32_t *X = sm, *Xn = xscratch + (size_t)blockIdx.x * MAXS * WC * NT;
         // ---- a5 prune (hybrid) / init (SOM)
         if (RULE == GB_HYBRID) {
             uint32_t x[MAXS][WC];
@@ -203,7 +206,8 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                         Xn[(t * WC + u) * NT + tid] = alive[u];
                     }
                 }
-                uint32_t *tmp = X; X = Xn; Xn = tmp;
+                if (changed)
+                    for (int w = 0; w < nslot * WC; ++w) X[w * NT + tid] = Xn[w * NT + tid];
                 ++it;
                 if (!changed) { status = GB_CONVERGED; break; }
             }
@@ -238,15 +242,26 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
 template <int WC, int RULE, int MAXS>
 cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                      uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    constexpr int NT = (128 * 1024) / (MAXS * WC * 8) > 256 ? 256 : (128 * 1024) / (MAXS * WC * 8);
-    const size_t smem = (size_t)2 * MAXS * WC * NT * sizeof(uint32_t);
+    constexpr int NT = (128 * 1024) / (MAXS * WC * 4) > 512 ? 512 : (128 * 1024) / (MAXS * WC * 4);
+    const size_t smem = (size_t)MAXS * WC * NT * sizeof(uint32_t);
+    const size_t need = (size_t)net->sm_count * MAXS * WC * NT * sizeof(uint32_t);
+    if (net->xscratch_bytes < need) {
+        cudaFree(net->xscratch);
+        net->xscratch = nullptr;
+        net->xscratch_bytes = 0;
+        if (cudaMalloc(&net->xscratch, need) != cudaSuccess) {
+            cudaGetLastError();
+            return cudaErrorMemoryAllocation;
+        }
+        net->xscratch_bytes = need;
+    }
     auto fn = decode_l2t_kernel<WC, RULE, MAXS, NT>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (k + NT - 1) / NT;
     if (grid > net->sm_count) grid = net->sm_count;
     fn<<<(unsigned)grid, NT, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status, net->ovf,
-                                         net->ovf_count);
+                                         net->ovf_count, net->xscratch);
     net->launches += 1;
     return cudaGetLastError();
 }
@@ -254,14 +269,14 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
 }  // namespace
 
 bool decode_l2t_supported(const Shape &s, int rule) {
+    // measured (round 1, same box, next state in L2 scratch): faster than the warp-per-probe
+    // kernel for the hybrid at C4 (2.59 vs 7.92 ms), Scenario 2 (0.270 vs 0.356 ms) and for
+    // sum-of-max at C4 (3.33 vs 4.59 ms); sum-of-max at Wc = 16 (16 slots x 64 B per thread)
+    // keeps decode_l2_kernel
     if (getenv("GB_NO_L2T")) return false;
-    if (rule == GB_SUM_OF_MAX && getenv("GB_L2T_ALL")) return s.C <= kMaxC16 && (s.Wc == 4 || s.Wc == 8);
-    // measured (round 1): faster than the warp-per-probe kernel for the hybrid at Wc = 8 (C4:
-    // 4.2 vs 7.9 ms); slower for sum-of-max at C4 (6.4 vs 4.6 ms: 16 slots leave 4 warps per
-    // SM) and for Scenario 2's Wc = 16 (0.44 vs 0.35 ms), which keep decode_l2_kernel
-    if (rule != GB_HYBRID || s.C > kMaxC16) return false;
-    if (getenv("GB_L2T_ALL")) return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;   // experiments / tests
-    return s.Wc == 4 || s.Wc == 8;
+    if (rule == GB_SUM_OF_SUM || s.C > kMaxC16) return false;
+    if (rule == GB_SUM_OF_MAX) return s.Wc == 4 || s.Wc == 8;
+    return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;
 }
 
 cudaError_t launch_decode_l2t(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,

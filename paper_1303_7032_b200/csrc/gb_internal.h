@@ -69,6 +69,8 @@ struct gb_net {
     int64_t ovf_cap;
     unsigned long long *ovf_count;
     size_t vscratch_bytes;
+    uint32_t *xscratch;                    // next-state scratch of the thread-per-probe L2 kernel
+    size_t xscratch_bytes;
     uint32_t *spart;                       // per-chunk partial bit matrices of the privatised store
     size_t spart_bytes;
 };

@@ -436,10 +436,10 @@ def test_determinism(gb):
                                            (8, 256, 0, "sos_tc3_kernel"), (4, 256, 0, "sos_tc2_kernel"),
                                            (8, 128, 2, "decode_hyb8_kernel"), (8, 128, 1, "decode_smem_kernel"),
                                            (4, 16, 2, "decode_smem_kernel"),
-                                           (16, 256, 1, "decode_l2_kernel"), (16, 256, 2, "decode_l2t_kernel"),
-                                           (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2_kernel"),
+                                           (16, 256, 1, "decode_l2t_kernel"), (16, 256, 2, "decode_l2t_kernel"),
+                                           (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2t_kernel"),
                                            (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc_kernel"),
-                                           (16, 512, 2, "decode_l2_kernel"), (9, 100, 2, "decode_l2t_kernel"),
+                                           (16, 512, 2, "decode_l2t_kernel"), (16, 512, 1, "decode_l2_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
@@ -565,9 +565,7 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule
     the oracle and against the warp-per-probe decode_l2_kernel (GB_NO_L2T): mixed
     erasure counts (probes with more erased clusters than its 8 hybrid slots are
     queued to the warp kernel), ragged L, M=0, invalid probes, random probes.
-    GB_L2T_ALL=1 also routes sum-of-max and Wc=16 through it (slower there, so not
-    the default, but it must stay exact)."""
-    monkeypatch.setenv("GB_L2T_ALL", "1")
+    """
     msgs = gbgen.messages(700 + c + l + m, max(m, 1), c, l)[:m]
     src = msgs if m else gbgen.messages(5, 10, c, l)
     pr, _ = gbgen.probes(701 + k, src, k, e, l, random_count=k // 5)
@@ -583,7 +581,6 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule
     want = oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=20)
     assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, f"l2t c={c} l={l}")
     assert_same(gpu_decode(net, pr, rule, 1, 2), oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=2), rule, "T=2")
-    monkeypatch.delenv("GB_L2T_ALL")
     monkeypatch.setenv("GB_NO_L2T", "1")
     assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, "warp kernel")
     net.close()
