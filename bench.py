@@ -98,13 +98,15 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def ncu_traffic(kernel, workload):
+def ncu_entry(kernel, workload):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
-        return None
-    d = json.load(open(p))
-    ent = d.get(f"{kernel}|{workload}")
-    return None if ent is None else ent.get("dram_bytes_per_launch")
+        return {}
+    return json.load(open(p)).get(f"{kernel}|{workload}", {})
+
+
+def ncu_traffic(kernel, workload):
+    return ncu_entry(kernel, workload).get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -467,6 +469,17 @@ def main():
                 "algorithmic_bytes_per_probe": bytes_per_probe,
                 "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
                 "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
+        wpp = ncu_entry(kernel, args.config).get("smem_wavefronts_per_probe")
+        if wpp:
+            # the binding on-chip resource of the bit kernels: shared-memory wavefronts through the
+            # LSU data pipe (one wavefront per SM per clock); per-probe count from the ncu capture
+            sm_clk = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+            per_s = wpp * k / (dec_ms / 1e3)
+            peak_wf = torch.cuda.get_device_properties(dev).multi_processor_count * sm_clk * 1e6
+            roof["onchip"] = {"resource": "shared-memory wavefronts (LSU data pipe, 1 per SM per clock)",
+                              "wavefronts_per_probe": wpp, "achieved_per_s": per_s, "peak_per_s": peak_wf,
+                              "frac": per_s / peak_wf, "source": ncu_entry(kernel, args.config).get("source")}
 
     # e2e through the C-ABI with pinned host buffers
     e2e = None

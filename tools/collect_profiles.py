@@ -47,6 +47,8 @@ def to_bytes(u, v):
     return float(v.replace(",", "")) * scale.get(u, 1)
 
 
+# probes per launch of the captures whose shared-memory wavefronts are reported per probe
+PROBES = {"prof_hyb": 10_000_000, "prof_l2": 1_000_000}
 traffic = {}
 for cap, (name, cfg) in CAPS.items():
     rep = os.path.join(G, f"{cap}_{TAG}.ncu-rep")
@@ -64,6 +66,10 @@ for cap, (name, cfg) in CAPS.items():
         b = to_bytes(*d["dram__bytes_read.sum"]) + to_bytes(*d["dram__bytes_write.sum"])
         traffic[tkey] = {"dram_bytes_per_launch": b, "source": f"profiles/{RND}_ncu_{name}.txt",
                          "note": "ncu --set full, one launch, --clock-control none"}
+        if cap in PROBES and "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum" in d:
+            wf = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][1].replace(",", ""))
+            traffic[tkey]["smem_wavefronts_per_probe"] = wf / PROBES[cap]
+            traffic[tkey]["probes_in_capture"] = PROBES[cap]
 if traffic:
     json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 for src, dst in ((f"bench_full_{TAG}.json", f"{RND}_bench_c3.json"),
