@@ -411,6 +411,10 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
 }
 
 constexpr int kWideThreads = 640;     // MAXS = 8
+#ifndef GB_SOM_THREADS
+#define GB_SOM_THREADS 768
+#endif
+constexpr int kSomThreads = GB_SOM_THREADS;   // sum-of-max instance (MAXS = 8)
 constexpr int kNarrowThreads = GB_NARROW_THREADS;   // MAXS = 4
 
 size_t smem_bytes(const Shape &s, int wc, int maxs, int nt) {
@@ -438,7 +442,10 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
 template <int WC, int RULE>
 cudaError_t launch_rule(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                         uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    if (RULE == GB_SUM_OF_MAX || net->s.C <= 4)   // every probe may need all C slots
+    if (RULE == GB_SUM_OF_MAX)   // every probe needs all C slots
+        return launch_t<WC, RULE, 8, kSomThreads>(net, probes, k, max_iters, state, iters, status, nullptr,
+                                                  nullptr, nullptr, nullptr, st);
+    if (net->s.C <= 4)
         return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, nullptr,
                                                    nullptr, nullptr, nullptr, st);
     // hybrid: probes with e <= 4 on the narrow (more threads) instance, the rest queued
@@ -472,6 +479,7 @@ bool decode_smem_supported(const Shape &s, int rule) {
     if (s.C > kMaxC || s.np > 1024 || rule == GB_SUM_OF_SUM) return false;
     if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4) return false;
     return smem_bytes(s, s.Wc, 8, kWideThreads) <= 227 * 1024 &&
+           smem_bytes(s, s.Wc, 8, kSomThreads) <= 227 * 1024 &&
            smem_bytes(s, s.Wc, 4, kNarrowThreads) <= 227 * 1024;
 }
 
