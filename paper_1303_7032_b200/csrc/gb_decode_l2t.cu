@@ -242,7 +242,13 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
 template <int WC, int RULE, int MAXS>
 cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                      uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    constexpr int NT = (128 * 1024) / (MAXS * WC * 4) > 512 ? 512 : (128 * 1024) / (MAXS * WC * 4);
+    // threads per CTA: as many slot-state columns as 192 KiB of shared memory hold (128 KiB at
+    // Wc = 16), at most 640 (register budget).  Same-box A/B: 128 KiB / 512 ->
+    // 192 KiB / 640 took C4 hybrid 2.59 -> 2.32 ms and C4 SOM 3.33 -> 2.32 ms; Scenario 2
+    // (Wc = 16) was faster at 128 KiB (0.270 vs 0.289 ms).
+    constexpr int kSmemKB = WC >= 16 ? 128 : 192;
+    constexpr int NT0 = (kSmemKB * 1024) / (MAXS * WC * 4);
+    constexpr int NT = (NT0 > 640 ? 640 : NT0) / 32 * 32;
     const size_t smem = (size_t)MAXS * WC * NT * sizeof(uint32_t);
     const size_t need = (size_t)net->sm_count * MAXS * WC * NT * sizeof(uint32_t);
     if (net->xscratch_bytes < need) {
