@@ -116,60 +116,8 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                     em &= em - 1u;
                 }
             }
-#ifndef GB_HYB8_GREEDY
-#define GB_HYB8_GREEDY 0
-#endif
-#if GB_HYB8_GREEDY
-            // greedy rotation per quarter-warp: lanes decide in order j = 0..7, each taking the
-            // rotation whose targets are least used so far at every step (counts per step and
-            // cluster as nibbles, quarter-uniform); the 8 lanes evaluate the decider's 4
-            // rotations x 2 steps in parallel
-            uint32_t rot = 0;
-            {
-                const uint32_t mine = ((work ? nslot : 0u) << 16) | slots;
-                uint32_t T0 = 0, T1 = 0, T2 = 0, T3 = 0;
-                const uint32_t rr = sw & 3u, t0 = (sw >> 2) * 2u;
-                const int qbase = lane & ~7;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t dl = __shfl_sync(0xffffffffu, mine, qbase | j);
-                    const uint32_t dn = dl >> 16;
-                    uint32_t part = 0;
-#pragma unroll
-                    for (int tt = 0; tt < 2; ++tt) {
-                        const uint32_t t = t0 + tt;
-                        if (t < dn && rr < dn) {
-                            uint32_t ix = t + rr;
-                            if (ix >= dn) ix -= dn;
-                            const uint32_t c = (dl >> (4 * ix)) & 15u;
-                            const uint32_t Tt = t == 0 ? T0 : t == 1 ? T1 : t == 2 ? T2 : T3;
-                            part += (Tt >> (4 * c)) & 15u;
-                        }
-                    }
-                    const uint32_t cost = part + __shfl_xor_sync(0xffffffffu, part, 4);
-                    uint32_t key = (rr < dn) ? ((cost << 2) | rr) : 0xffffu;
-                    key = min(key, __shfl_xor_sync(0xffffffffu, key, 1));
-                    key = min(key, __shfl_xor_sync(0xffffffffu, key, 2));
-                    const uint32_t best = key & 3u;
-                    if (sw == (uint32_t)j) rot = best;
-#pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        if ((uint32_t)t < dn) {
-                            uint32_t ix = t + best;
-                            if (ix >= dn) ix -= dn;
-                            const uint32_t inc = 1u << (4 * ((dl >> (4 * ix)) & 15u));
-                            if (t == 0) T0 += inc;
-                            else if (t == 1) T1 += inc;
-                            else if (t == 2) T2 += inc;
-                            else T3 += inc;
-                        }
-                    }
-                }
-            }
-#else
             const uint32_t tab = nslot == 4 ? 0x32103210u : nslot == 3 ? 0x10210210u : nslot == 2 ? 0x10101010u : 0u;
             const uint32_t rot = (tab >> (4 * sw)) & 15u;
-#endif
             if (rot) {
                 const uint32_t bits = 4u * nslot;
                 slots = ((slots >> (4u * rot)) | (slots << (bits - 4u * rot))) & ((1u << bits) - 1u);
