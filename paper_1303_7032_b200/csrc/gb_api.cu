@@ -120,19 +120,19 @@ int gb_create(int c, int l, int device, gb_net **out) {
     net->sm_count = prop.multiProcessorCount;
     const size_t w8b = (size_t)s.np * s.np, wbb = (size_t)s.np * s.nw * sizeof(uint32_t);
     if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb) != cudaSuccess ||
-        cudaMalloc(&net->dflag, sizeof(unsigned)) != cudaSuccess ||
-        cudaMalloc(&net->dcount, sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&net->dcount, 16) != cudaSuccess ||   // [0, 8) invalid-message count, [8, 12) flags
+        cudaMallocHost(&net->hstat, 16) != cudaSuccess ||
         cudaMalloc(&net->queue, sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&net->ovf_count, sizeof(unsigned long long)) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dflag); cudaFree(net->dcount); cudaFree(net->queue); cudaFree(net->ovf_count);
+        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dcount); cudaFreeHost(net->hstat); cudaFree(net->queue); cudaFree(net->ovf_count);
         free(net);
         return fail(GB_ENOMEM, "gb_create: device allocation of W (%zu bytes)", w8b + wbb);
     }
     cudaMemset(net->w8, 0, w8b);
     cudaMemset(net->wb, 0, wbb);
-    cudaMemset(net->dflag, 0, sizeof(unsigned));
-    cudaMemset(net->dcount, 0, sizeof(unsigned long long));
+    net->dflag = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(net->dcount) + 8);
+    cudaMemset(net->dcount, 0, 16);
     for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&net->stage_stream[i], cudaStreamNonBlocking);
     for (int i = 0; i < 4; ++i) cudaEventCreateWithFlags(&net->stage_event[i], cudaEventDisableTiming);
     cudaError_t e = cudaDeviceSynchronize();
@@ -156,8 +156,8 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->vscratch);
     cudaFree(net->w8);
     cudaFree(net->wb);
-    cudaFree(net->dflag);
-    cudaFree(net->dcount);
+    cudaFree(net->dcount);   // also holds dflag
+    cudaFreeHost(net->hstat);
     cudaFree(net->queue);
     cudaFree(net->ovf);
     cudaFree(net->ovf_count);
@@ -172,8 +172,7 @@ int gb_clear(gb_net *net, void *stream) {
     DeviceGuard g(net->device);
     cudaStream_t st = (cudaStream_t)stream;
     GB_CUDA(cudaMemsetAsync(net->w8, 0, (size_t)net->s.np * net->s.np, st), "gb_clear");
-    GB_CUDA(cudaMemsetAsync(net->dflag, 0, sizeof(unsigned), st), "gb_clear");
-    GB_CUDA(cudaMemsetAsync(net->dcount, 0, sizeof(unsigned long long), st), "gb_clear");
+    GB_CUDA(cudaMemsetAsync(net->dcount, 0, 16, st), "gb_clear");   // count + flags
     net->stored = 0;
     net->sealed = false;
     return GB_OK;
@@ -244,11 +243,12 @@ int gb_seal(gb_net *net, void *stream) {
     net->launches += 1;
     unsigned flag = 0;
     unsigned long long cnt = 0;
-    GB_CUDA(cudaMemcpyAsync(&flag, net->dflag, sizeof flag, cudaMemcpyDeviceToHost, st), "gb_seal: flag");
-    GB_CUDA(cudaMemcpyAsync(&cnt, net->dcount, sizeof cnt, cudaMemcpyDeviceToHost, st), "gb_seal: count");
+    // count and flags in one 16-byte copy to pinned memory, then one reset
+    GB_CUDA(cudaMemcpyAsync(net->hstat, net->dcount, 16, cudaMemcpyDeviceToHost, st), "gb_seal: status");
     GB_CUDA(cudaStreamSynchronize(st), "gb_seal: sync");
-    GB_CUDA(cudaMemsetAsync(net->dflag, 0, sizeof(unsigned), st), "gb_seal: reset");
-    GB_CUDA(cudaMemsetAsync(net->dcount, 0, sizeof(unsigned long long), st), "gb_seal: reset");
+    memcpy(&cnt, net->hstat, sizeof cnt);
+    memcpy(&flag, reinterpret_cast<const char *>(net->hstat) + 8, sizeof flag);
+    GB_CUDA(cudaMemsetAsync(net->dcount, 0, 16, st), "gb_seal: reset");
     const unsigned structural = flag & ~gb::kFlagStoreInvalid;
     if (structural) {
         net->sealed = false;

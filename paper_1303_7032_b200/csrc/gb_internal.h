@@ -39,8 +39,9 @@ struct gb_net {
     int sm_count;
     uint8_t *w8;          // [np][np] u8, row-major
     uint32_t *wb;         // [np][nw] bit rows
-    unsigned *dflag;      // device error flags
-    unsigned long long *dcount;  // [0] invalid stored messages
+    unsigned long long *dcount;  // 16-byte device status: [0, 8) invalid stored messages,
+    unsigned *dflag;             // [8, 12) error flags (dflag points into the same allocation)
+    void *hstat;                 // 16-byte pinned copy of the status (gb_seal)
     int64_t stored;
     bool sealed;
     // host-staging scratch (gb_decode / gb_store with host pointers)
