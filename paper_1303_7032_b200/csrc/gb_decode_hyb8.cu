@@ -344,8 +344,14 @@ static bool encode_out_map(void *state, int64_t k, CUtensorMap *map) {
 // to net->ovf for decode_smem_kernel's list mode (launched by the caller).
 cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                                uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    alignas(64) CUtensorMap map;
-    if (!encode_out_map(state, k, &map)) return cudaErrorNotSupported;
+    // the output tensor map depends only on (out_state, k): reuse it across calls
+    CUtensorMap &map = *reinterpret_cast<CUtensorMap *>(net->omap);
+    if (!net->omap_ok || net->omap_ptr != state || net->omap_k != k) {
+        net->omap_ok = encode_out_map(state, k, &map);
+        net->omap_ptr = state;
+        net->omap_k = k;
+        if (!net->omap_ok) return cudaErrorNotSupported;
+    }
     auto fn = decode_hyb8_kernel;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;

@@ -60,6 +60,10 @@ struct gb_net {
     alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
     bool wmap_g3_ok;
     int wmap_g3_br;                          // box rows wmap_g3 was encoded with
+    alignas(64) unsigned char omap[128];     // out_state map of decode_hyb8_kernel (cached per buffer, k)
+    bool omap_ok;
+    const void *omap_ptr;
+    int64_t omap_k;
     alignas(64) unsigned char wmap_som[128]; // W8 map for the tensor-core sum-of-max kernel
     bool wmap_som_ok;
     int w8g_gamma;
