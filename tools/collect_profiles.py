@@ -48,7 +48,7 @@ def to_bytes(u, v):
 
 
 # probes per launch of the captures whose shared-memory wavefronts are reported per probe
-PROBES = {"prof_hyb": 10_000_000, "prof_l2": 1_000_000}
+PROBES = {"prof_hyb": 10_000_000}   # kernels whose W rows live in shared memory
 traffic = {}
 for cap, (name, cfg) in CAPS.items():
     rep = os.path.join(G, f"{cap}_{TAG}.ncu-rep")
