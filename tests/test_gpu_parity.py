@@ -488,6 +488,57 @@ def test_config4_full_size_sampled(gb):
                     "config4 sampled")
 
 
+def test_config4_hybrid_full_size_sampled(gb):
+    """BASELINE config 4 hybrid at the bench's size (c=16 l=256, M=10^5, e=8,
+    K=10^6, decode_l2t_kernel): 24 sampled probes vs the oracle, plus over all K:
+    no invalid status, known clusters one-hot, every stored source message
+    contained in its final state (Lemma 3)."""
+    c, l, m, k = 16, 256, 100_000, 1_000_000
+    msgs = gbgen.messages(0x5EED, m, c, l)
+    pr, src = gbgen.probes(0x5EED + 1, msgs, k, 8, l)
+    net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(2) == "decode_l2t_kernel"
+    st, it, ss = net.decode(to_dev(pr), 2, gamma=2, max_iters=20)
+    torch.cuda.synchronize()
+    assert int((ss == 2).sum()) == 0
+    wc = 8
+    msg_d = torch.from_numpy(msgs[src].astype(np.int64)).cuda()
+    cols = torch.arange(c, device="cuda") * wc + (msg_d >> 5)
+    words = torch.gather(st, 1, cols).to(torch.int64) & 0xFFFFFFFF
+    bit = torch.bitwise_left_shift(torch.ones_like(msg_d), msg_d & 31)
+    assert bool((words & bit).ne(0).all())
+    known = torch.from_numpy(pr.astype(np.int64)).cuda() != 0xFFFF
+    only = words.eq(bit) | ~known          # a known cluster's word holds exactly the probe's bit
+    assert bool(only.all())
+    rng = np.random.default_rng(4)
+    idx = np.sort(rng.choice(k, 24, replace=False))
+    w, _ = oracle.store(msgs, c, l)
+    want = oracle.decode(w, c, l, pr[idx], 2, gamma=2, max_iters=20)
+    got = (st[idx].cpu().numpy().view(np.uint32), it[idx].cpu().numpy().view(np.uint16), ss[idx].cpu().numpy())
+    assert_same(got, want, 2, "config4 hybrid sampled")
+
+
+def test_config5_full_size_store(gb):
+    """BASELINE config 5 at full size: 10^7 messages at c=16 l=256 stored by the
+    privatised kernel in one call, and as 4 shards merged by the packed OR
+    (gb_bits + gb_or_bits, the N3 merge) -- both equal the oracle's W (Eq.(1))
+    byte for byte."""
+    c, l, m = 16, 256, 10_000_000
+    msgs = gbgen.messages(0x5EED, m, c, l)
+    w, bad = oracle.store(msgs, c, l)
+    assert bad == 0
+    want = padded_w(w, c, l)
+    net = make_net(gb, msgs, c, l)
+    np.testing.assert_array_equal(net.weights().cpu().numpy(), want)
+    parts = [make_net(gb, msgs[i::4], c, l) for i in range(4)]
+    merged = gb.Net(c, l)
+    merged.or_bits(torch.stack([p_.bits() for p_ in parts]).contiguous())
+    merged.seal()
+    np.testing.assert_array_equal(merged.weights().cpu().numpy(), want)
+    for n in parts + [merged, net]:
+        n.close()
+
+
 def test_mixed_erasures_narrow_and_wide_slots(gb):
     """Hybrid probes with e <= 4 run on the 4-slot instance, the rest are queued to the
     8-slot instance (list mode) inside the same gb_decode; per-probe e from 0 to C in
