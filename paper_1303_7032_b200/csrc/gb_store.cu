@@ -21,6 +21,13 @@
 namespace gb {
 namespace {
 
+#ifndef GB_PRIV_TILE_KB
+#define GB_PRIV_TILE_KB 128
+#endif
+#ifndef GB_PRIV_NT
+#define GB_PRIV_NT 1024
+#endif
+
 __device__ __forceinline__ void st_relaxed_u8(uint8_t *p, unsigned v) {
     asm volatile("st.relaxed.gpu.global.u8 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -116,7 +123,7 @@ struct PrivPlan {
 };
 
 template <int NV>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(GB_PRIV_NT, 1)
 store_priv_kernel(Shape s, const uint16_t *__restrict__ msgs, int64_t m, int G, int ngroups, int tiles,
                   int64_t per_chunk, uint32_t *__restrict__ part, unsigned long long *__restrict__ dcount,
                   unsigned *__restrict__ dflag) {
@@ -218,7 +225,7 @@ __global__ void apply_kernel(Shape s, const uint32_t *__restrict__ part, int chu
     }
 }
 
-constexpr size_t kPrivTileMax = 128 * 1024;
+constexpr size_t kPrivTileMax = GB_PRIV_TILE_KB * 1024;
 
 PrivPlan priv_plan(const Shape &s, int64_t m, int sm_count) {
     PrivPlan p;
@@ -266,7 +273,7 @@ cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStrea
             : nv == 3 ? store_priv_kernel<3> : nv == 4 ? store_priv_kernel<4> : store_priv_kernel<0>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_bytes);
     if (e != cudaSuccess) return e;
-    fn<<<(unsigned)(p.chunks * p.tiles), 1024, p.tile_bytes, st>>>(
+    fn<<<(unsigned)(p.chunks * p.tiles), GB_PRIV_NT, p.tile_bytes, st>>>(
         s, msgs, m, p.G, p.ngroups, p.tiles, p.per_chunk, net->spart, net->dcount, net->dflag);
     const int64_t total = (int64_t)s.np * s.nw;
     apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, net->spart, p.chunks, net->w8);
