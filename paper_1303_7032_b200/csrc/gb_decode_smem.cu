@@ -1,6 +1,7 @@
 // gb_decode_smem.cu -- thread-per-probe SOM / hybrid decode with W held in
-// shared memory (n_padded <= 1024, C <= 8): the hot path of the metric
-// (hybrid rule, c=8 l=128).
+// shared memory (n_padded <= 1024, C <= 8): sum-of-max at the paper's shape,
+// the hybrid shapes decode_hyb8_kernel does not take (C != 8 or Wc != 4), and
+// the hybrid probes with e > 4 that it queues (8-slot instance, list mode).
 //
 // Layout (DESIGN.md §Kernels / "smem bit kernel"):
 //  * W bit rows copied once per CTA into shared memory (128 KiB at c=8
