@@ -710,3 +710,32 @@ def test_som_tensor_core_matches_oracle(gb, monkeypatch, c, l, m, e, k):
     assert net.decode_kernel(1) != "som_tc_kernel"
     assert_same(gpu_decode(net, pr, 1, 3, 20), oracle.decode(w, c, l, pr, 1, gamma=3, max_iters=20), 1, "bit")
     net.close()
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_random_shapes_fuzz(gb, seed):
+    """Seeded sweep over random shapes (C 2..16, L 1..300 incl. ragged and
+    non-power-of-two word counts), stored-message counts, erasure counts,
+    rules, gamma and max_iters: every kernel the selection can reach (pair /
+    streamed-A / 4-warp / generic SOS, hyb8 / smem / l2t / l2 / generic bit
+    kernels, both store kernels) against the oracle, bit for bit."""
+    rng = np.random.default_rng(1000 + seed)
+    for case in range(8):
+        c = int(rng.integers(2, 17))
+        l = int(rng.choice([1, 3, 16, 31, 33, 64, 70, 100, 128, 129, 200, 256, 300]))
+        if c * 32 * ((l + 31) // 32) > 8192 or c * l > 3000:
+            l = 64
+        m = int(rng.choice([0, 5, 50, 500, 3000]))
+        k = int(rng.integers(1, 300))
+        e = int(rng.integers(0, c + 1))
+        rule = int(rng.integers(0, 3))
+        gamma = int(rng.choice([0, 1, 2, 5])) if rule == 0 else int(rng.choice([1, 2, 7]))
+        T = int(rng.choice([1, 2, 5, 20]))
+        msgs = gbgen.messages(seed * 100 + case, max(m, 1), c, l)[:m]
+        src = msgs if m else gbgen.messages(3, 5, c, l)
+        pr, _ = gbgen.probes(seed * 100 + case + 1, src, k, e, l, random_count=k // 4)
+        w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
+        net = make_net(gb, msgs, c, l)
+        tag = f"fuzz c={c} l={l} m={m} k={k} e={e} rule={rule} g={gamma} T={T} kernel={net.decode_kernel(rule)}"
+        assert_same(gpu_decode(net, pr, rule, gamma, T), oracle.decode(w, c, l, pr, rule, gamma, T), rule, tag)
+        net.close()
