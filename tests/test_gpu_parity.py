@@ -739,3 +739,40 @@ def test_random_shapes_fuzz(gb, seed):
         tag = f"fuzz c={c} l={l} m={m} k={k} e={e} rule={rule} g={gamma} T={T} kernel={net.decode_kernel(rule)}"
         assert_same(gpu_decode(net, pr, rule, gamma, T), oracle.decode(w, c, l, pr, rule, gamma, T), rule, tag)
         net.close()
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_shapes_mixed_erasures_fuzz(gb, seed):
+    """Like the shape fuzz, but every probe has its own erasure count (wide-slot
+    and list-mode paths), some symbols are invalid, and SOS runs with the
+    period-2 cycle exit half of the time."""
+    rng = np.random.default_rng(5000 + seed)
+    for case in range(6):
+        c = int(rng.integers(2, 17))
+        l = int(rng.choice([2, 16, 32, 50, 96, 128, 130, 256]))
+        if c * 32 * ((l + 31) // 32) > 4096:
+            l = 32
+        m = int(rng.choice([5, 100, 2000]))
+        k = int(rng.integers(1, 400))
+        rule = int(rng.integers(0, 3))
+        gamma = int(rng.choice([0, 1, 2])) if rule == 0 else 1
+        flags = int(rule == 0 and rng.random() < 0.5)
+        T = int(rng.choice([2, 7, 20]))
+        msgs = gbgen.messages(seed * 50 + case, m, c, l)
+        pr, _ = gbgen.probes(seed * 50 + case + 1, msgs, k, 1, l, random_count=k // 3)
+        for i in range(k):
+            row = pr[i].copy()
+            row[row == 0xFFFF] = rng.integers(0, l)
+            row[rng.choice(c, int(rng.integers(0, c + 1)), replace=False)] = 0xFFFF
+            if rng.random() < 0.02:
+                row[int(rng.integers(0, c))] = l + int(rng.integers(0, 5))
+            pr[i] = row
+        w, _ = oracle.store(msgs, c, l)
+        net = make_net(gb, msgs, c, l)
+        st, it, ss = net.decode(to_dev(pr), rule, gamma=gamma, max_iters=T, flags=flags)
+        torch.cuda.synchronize()
+        got = (st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy())
+        want = oracle.decode(w, c, l, pr, rule, gamma, T, flags=flags)
+        assert_same(got, want, rule, f"mixed fuzz c={c} l={l} m={m} k={k} rule={rule} g={gamma} T={T} f={flags} "
+                                     f"kernel={net.decode_kernel(rule)}")
+        net.close()
