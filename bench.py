@@ -441,7 +441,7 @@ def main():
     hbm, bf16, peak_kind = measured_peaks()
     bytes_per_probe = 2 * c + 4 * nw + 2 + 1
     kernel = net.decode_kernel(rule)
-    if kernel.startswith("sos_tc"):
+    if kernel.startswith("sos_"):
         # tensor-bound.  Algorithmic int8 ops = sum over probes of its rounds x 2 n_p^2 (Eq.(11) per
         # probe-round).  Both SOS kernels refill converged slots of their 128-probe tiles, so the
         # executed work is the algorithmic work plus the last partial rounds (a fixed-tile kernel
@@ -452,15 +452,19 @@ def main():
         npad = net.n_padded
         ops_alg = float(it_h.sum()) * 2 * npad * npad
         ops_tile = float(tiles.sum()) * 2 * 128 * npad * npad
-        peak = 2.0 * bf16   # int8 dense = 2 x bf16 (guide's nominal 4.5 / 2.25 PFLOP/s) x measured bf16
+        fp4 = kernel.startswith("sos_fp4")
+        # int8 dense = 2 x bf16, e2m1 (block-scaled FP4) dense = 4 x bf16 (guide's nominal 4.5 / 9 vs
+        # 2.25 PFLOP/s) x the measured bf16 peak
+        peak = (4.0 if fp4 else 2.0) * bf16
         achieved = ops_alg / (dec_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS(int8)",
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TOPS(fp4)" if fp4 else "TOPS(int8)",
                 "frac": achieved / peak, "traffic": ncu_traffic(kernel, args.config), "kernel": kernel,
                 "ops_per_probe_round": 2 * npad * npad, "probe_rounds": int(it_h.sum()),
                 "tile_rounds_if_no_refill": int(tiles.sum()),
                 "ops_basis": "algorithmic (per-probe rounds); the kernels refill converged TMEM lanes, so "
                              "executed work = algorithmic + the partial last rounds",
-                "peak_source": peak_kind + " (2 x MEASURED_PEAKS.json bf16_tflops, int8/bf16 nominal ratio)",
+                "peak_source": peak_kind + (" (4 x MEASURED_PEAKS.json bf16_tflops, fp4/bf16 nominal ratio)" if fp4
+                                            else " (2 x MEASURED_PEAKS.json bf16_tflops, int8/bf16 nominal ratio)"),
                 "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
     else:
         achieved = k * bytes_per_probe / (dec_ms / 1e3) / 1e9

@@ -163,6 +163,7 @@ int gb_destroy(gb_net *net) {
     cudaFree(net->ovf_count);
     cudaFree(net->spart);
     cudaFree(net->xscratch);
+    cudaFree(net->w4);
     free(net);
     return GB_OK;
 }
@@ -349,6 +350,7 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
+    if (rule == GB_SUM_OF_SUM && gb::sos_fp4_enabled(net->s, 2)) return "sos_fp4_kernel";   // (gamma = 2)
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
         return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net->s))

@@ -786,6 +786,10 @@ cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k,
                                  int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
     Sos2Params P2;
     size_t smem2;
+    if (sos_fp4_enabled(net->s, gamma)) {   // exact 0/1 contraction on e2m1 (n_p <= 1024, Lp <= 128)
+        cudaError_t e = launch_sos_fp4(net, gamma, cyc, probes, k, max_iters, state, iters, status, st);
+        if (e != cudaErrorNotSupported) return e;
+    }
     if (sos_tc3_enabled(net->s)) {   // 1024 < n_p <= 4096: streamed A tile
         cudaError_t e = ensure_w8g(net, gamma, st);
         if (e != cudaSuccess) return e;

@@ -60,6 +60,10 @@ struct gb_net {
     alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
     bool wmap_g3_ok;
     int wmap_g3_br;                          // box rows wmap_g3 was encoded with
+    uint8_t *w4;                             // W8 + gamma*I as packed e2m1 (B operand of sos_fp4_kernel)
+    alignas(64) unsigned char w4map[128];
+    unsigned long long w4_gen;
+    int w4_gamma;
     alignas(64) unsigned char omap[128];     // out_state map of decode_hyb8_kernel (cached per buffer, k)
     bool omap_ok;
     const void *omap_ptr;
@@ -119,6 +123,10 @@ bool sos_tc3_pair(const Shape &s);   // the streamed-A kernel runs on CTA pairs
 cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 // cyc = 1: period-2 cycle exit (GB_FLAG_CYCLE_EXIT) in every sum-of-sum kernel
+// sum-of-sum on block-scaled FP4 tensor cores (gb_decode_sos_fp4.cu)
+bool sos_fp4_enabled(const Shape &s, int gamma);
+cudaError_t launch_sos_fp4(gb_net *net, int gamma, int cyc, const uint16_t *probes, int64_t k, int max_iters,
+                           uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
 // exact sum-of-max on the tensor cores (gb_decode_som_tc.cu, N2), opt-in with GB_SOM_TC=1
 bool som_tc_enabled(const Shape &s);
 cudaError_t launch_som_tc(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,

@@ -776,3 +776,33 @@ def test_random_shapes_mixed_erasures_fuzz(gb, seed):
         assert_same(got, want, rule, f"mixed fuzz c={c} l={l} m={m} k={k} rule={rule} g={gamma} T={T} f={flags} "
                                      f"kernel={net.decode_kernel(rule)}")
         net.close()
+
+
+@pytest.mark.parametrize("c,l,m,e,gamma,k", [(8, 128, 5000, 4, 2, 1000), (8, 128, 30000, 5, 1, 700),
+                                             (4, 16, 50, 2, 6, 300), (3, 3, 4, 2, 1, 1), (5, 60, 2000, 3, 0, 257),
+                                             (7, 100, 3000, 3, 4, 129), (16, 64, 3000, 9, 3, 200)])
+def test_sos_fp4_matches_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
+    """Sum-of-sum on block-scaled FP4 tensor cores (kind::mxf4, opt-in GB_SOS_FP4=1):
+    V, W in {0, 1} and gamma in {0, 1, 2, 3, 4, 6} are e2m1 values, so with unit
+    scales the fp32 sums are the exact integer scores -- bit-exact vs the oracle
+    (states, rounds, statuses), also with the cycle-exit flag; ragged L and
+    n_p not a multiple of the 256-neuron K block."""
+    monkeypatch.setenv("GB_SOS_FP4", "1")
+    if m == 4:
+        msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
+        pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
+    else:
+        msgs = gbgen.messages(1100 + c + l, m, c, l)
+        pr, _ = gbgen.probes(1101 + c, msgs, k, e, l, random_count=k // 5)
+        pr[0, 0] = l
+    w, _ = oracle.store(msgs, c, l)
+    net = make_net(gb, msgs, c, l)
+    if gamma == 2:
+        assert net.decode_kernel(0) == "sos_fp4_kernel"
+    for T in (20, 3):
+        assert_same(gpu_decode(net, pr, 0, gamma, T), oracle.decode(w, c, l, pr, 0, gamma, T), 0, f"fp4 T={T}")
+    st, it, ss = net.decode(to_dev(pr), 0, gamma=gamma, max_iters=20, flags=gb.FLAG_CYCLE_EXIT)
+    torch.cuda.synchronize()
+    got = (st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy())
+    assert_same(got, oracle.decode(w, c, l, pr, 0, gamma, 20, flags=oracle.CYCLE_EXIT), 0, "fp4 cycle")
+    net.close()
