@@ -249,6 +249,12 @@ int gb_seal(gb_net *net, void *stream) {
     GB_CUDA(cudaStreamSynchronize(st), "gb_seal: sync");
     memcpy(&cnt, net->hstat, sizeof cnt);
     memcpy(&flag, reinterpret_cast<const char *>(net->hstat) + 8, sizeof flag);
+    unsigned edges = 0;
+    memcpy(&edges, reinterpret_cast<const char *>(net->hstat) + 12, sizeof edges);
+    {
+        const double pairs = (double)net->s.C * (net->s.C - 1) * (double)net->s.L * net->s.L;
+        net->density = pairs > 0 ? edges / pairs : 0.0;
+    }
     GB_CUDA(cudaMemsetAsync(net->dcount, 0, 16, st), "gb_seal: reset");
     const unsigned structural = flag & ~gb::kFlagStoreInvalid;
     if (structural) {

@@ -40,8 +40,10 @@ struct gb_net {
     uint8_t *w8;          // [np][np] u8, row-major
     uint32_t *wb;         // [np][nw] bit rows
     unsigned long long *dcount;  // 16-byte device status: [0, 8) invalid stored messages,
-    unsigned *dflag;             // [8, 12) error flags (dflag points into the same allocation)
+    unsigned *dflag;             // [8, 12) error flags (dflag points into the same allocation),
+                                 // [12, 16) edge count of W (both directions, counted by seal)
     void *hstat;                 // 16-byte pinned copy of the status (gb_seal)
+    double density;              // edges / (C (C-1) L^2) of the sealed W (kernel heuristics)
     int64_t stored;
     bool sealed;
     // host-staging scratch (gb_decode / gb_store with host pointers)

@@ -76,7 +76,7 @@ __device__ __forceinline__ uint32_t pack32(const uint8_t *p, unsigned &nonbin) {
 }
 
 __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *__restrict__ wb,
-                            unsigned *__restrict__ dflag) {
+                            unsigned *__restrict__ dflag, unsigned *__restrict__ dedges) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nt = s.np / 32;
@@ -103,6 +103,8 @@ __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *_
     wb[(int64_t)(i0 + lane) * s.nw + tj] = P;
     const unsigned anybad = __reduce_or_sync(0xffffffffu, bad);
     if (lane == 0 && anybad) atomicOr(dflag, anybad);
+    const unsigned ne = __reduce_add_sync(0xffffffffu, (unsigned)__popc(P));   // edges (both directions)
+    if (lane == 0 && ne) atomicAdd(dedges, ne);
 }
 
 // ---- privatised store (large m): one CTA = (row cluster c, column-cluster
@@ -293,7 +295,7 @@ cudaError_t launch_seal(const gb_net *net, cudaStream_t st) {
     const int64_t warps = (int64_t)(net->s.np / 32) * (net->s.np / 32);
     const int block = 256;
     const int64_t grid = (warps * 32 + block - 1) / block;
-    seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dflag);
+    seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dflag, net->dflag + 1);
     return cudaGetLastError();
 }
 

@@ -185,6 +185,10 @@ def test_hyb8_matches_oracle_and_generic(gb, monkeypatch, l, m, k):
     assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "T=3")
     monkeypatch.delenv("GB_NO_HYB8")
     assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "hyb8 T=3")
+    for split in ("0", "1"):                        # stage 2 whole / in two halves (density heuristic forced)
+        monkeypatch.setenv("GB_HYB8_SPLIT2", split)
+        assert_same(gpu_decode(net, pr, 2, 1, 20), want, 2, f"hyb8 split2={split}")
+    monkeypatch.delenv("GB_HYB8_SPLIT2")
     net.close()
 
 

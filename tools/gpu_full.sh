@@ -21,4 +21,5 @@ rm -f gpurun_out/bench_rules_$TAG.jsonl
 for a in "--config c2 --rule 0" "--config c2 --rule 1" "--config c2 --rule 2" "--config c2 --rule 0 --probes 1000000" "--config c2 --rule 2 --probes 10000000" "--config c4 --rule 0 --probes 100000" "--config c4 --rule 1 --probes 100000" "--config c4 --rule 2" "--config c1 --rule 2" "--config s2 --rule 2" "--config s2 --rule 0" "--config c5"; do
   timeout 300 python bench.py --no-cpu --no-e2e --steps 10 $a >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
 done
+GB_SOS_FP4=1 timeout 300 python bench.py --no-cpu --no-e2e --steps 10 --config c2 --rule 0 --probes 1000000 >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
 ls gpurun_out | tail -20

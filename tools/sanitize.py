@@ -2,7 +2,7 @@
 
 Covers every kernel family: store (scattered + privatised) + apply + seal, OR of packed
 partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l2 (list mode),
-SOS pair / streamed-A / 4-warp / generic, the cycle-exit flag, and the tensor-core SOM kernel.
+SOS pair / streamed-A / 4-warp / generic / FP4, the cycle-exit flag, and the tensor-core SOM kernel.
 """
 import os
 import sys
@@ -31,6 +31,14 @@ for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 50
         os.environ["GB_SOM_TC"] = "1"
         net.decode(probes, 1, gamma=1, max_iters=6)
         del os.environ["GB_SOM_TC"]
+        os.environ["GB_SOS_FP4"] = "1"
+        net.decode(probes, 0, gamma=2, max_iters=6)
+        net.decode(probes, 0, gamma=0, max_iters=6, flags=gb.FLAG_CYCLE_EXIT)
+        del os.environ["GB_SOS_FP4"]
+        for split in ("0", "1"):
+            os.environ["GB_HYB8_SPLIT2"] = split
+            net.decode(probes, 2, gamma=1, max_iters=6)
+        del os.environ["GB_HYB8_SPLIT2"]
         part = gb.Net(c, l)
         part.store(torch.from_numpy(msgs[: m // 2].view(np.int16)).cuda())
         part.seal()
