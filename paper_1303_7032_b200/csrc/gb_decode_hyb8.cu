@@ -50,9 +50,10 @@ __device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
 
+template <bool SPLIT2>
 __global__ void __launch_bounds__(kNT, 1)
 decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
-                   int T, int split2, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
+                   int T, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
                    uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
                    unsigned long long *__restrict__ ovf_count) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -208,7 +209,7 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                     // stage 2: the highest other candidate of each word holding >= 2
 #pragma unroll
                                     for (int u = 0; u < 4; ++u) {
-                                        if (u == 2 && split2) {   // dense W: check before words 2, 3
+                                        if (SPLIT2 && u == 2) {   // dense W: check before words 2, 3
                                             miss = 0u;
 #pragma unroll
                                             for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
@@ -363,13 +364,13 @@ cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, i
     // reach stage 2 and two more rows usually cover): same-box A/B at C3 (density 0.70)
     // 1.109 -> 1.053 ms, at C2 (density 0.26) 3.33 -> 3.59 ms.  GB_HYB8_SPLIT2=0/1 forces it.
     const char *fs = getenv("GB_HYB8_SPLIT2");
-    const int split2 = fs ? (atoi(fs) != 0) : (net->density > 0.5);
-    auto fn = decode_hyb8_kernel;
+    const bool split2 = fs ? (atoi(fs) != 0) : (net->density > 0.5);
+    auto fn = split2 ? decode_hyb8_kernel<true> : decode_hyb8_kernel<false>;   // compile-time: no cost when off
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
     int64_t grid = (k + kNT - 1) / kNT;
     if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, kNT, kSmem, st>>>(net->wb, probes, k, net->s.L, max_iters, split2, map, iters,
+    fn<<<(unsigned)grid, kNT, kSmem, st>>>(net->wb, probes, k, net->s.L, max_iters, map, iters,
                                                             status, net->ovf, net->ovf_count);
     net->launches += 1;
     return cudaGetLastError();
