@@ -336,7 +336,7 @@ def main():
                     help="C5 store merge over ranks: packed all-gather + OR (N3) or u8 MAX all-reduce")
     ap.add_argument("--max-iters", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--cpu-budget", type=float, default=18.0)   # calibration on 256 probes overestimates the time (~0.7x measured)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
