@@ -13,8 +13,10 @@ Parity status per function (DESIGN.md §"Oracle pins"):
                Python-set edge count; density closed form 1-(1-1/L^2)^M.
   decode SOS   pinned: PAPER.md L515-522 trajectory (gamma=1), gamma=2
                convergence (L525), numpy score identity, fixed points,
-               single-clique and M=0 closed cases.  Large random instances:
-               literal definition only (no independent closed form).
+               single-clique and M=0 closed cases; on random instances at the
+               Scenario-1 shape every round equals the library contraction
+               (W + gamma I) V + per-cluster max/== and the stopping rule of
+               Alg. 1 (test_sos_decode_is_composed_library_rounds).
   decode SOM   pinned: Thm 1 (Python bail-out-early), gamma invariance,
                brute-force greatest self-supporting subset, Lemmas 1-3,
                PAPER.md L668-669 pool example.

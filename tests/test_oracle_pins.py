@@ -227,6 +227,41 @@ def test_sos_score_is_library_matmul(gamma):
         np.testing.assert_array_equal(v[1].reshape(c, l), (blk == blk.max(axis=1, keepdims=True)))
 
 
+@pytest.mark.parametrize("c,l,m,e,gamma", [(8, 128, 5000, 4, 2), (8, 128, 5000, 5, 1), (4, 16, 60, 2, 0),
+                                           (6, 40, 900, 3, 3)])
+def test_sos_decode_is_composed_library_rounds(c, l, m, e, gamma):
+    """Alg. 1 end to end on random instances at the Scenario-1
+    shape: the oracle's SOS decode equals rounds of the library contraction
+    S = (W + gamma I) V (numpy int64 matmul, Eq.(10)-(11)) followed by the
+    per-cluster max / == selection (Eq.(4)-(5)), started from V^0 = known
+    one-hot, erased 0 and stopped at the first round with
+    V^{t+1} == V^t (iters = that round, CONVERGED) or after T rounds
+    (MAX_ITERS).  Pins the multi-round trajectories and the stopping rule, not
+    only one round."""
+    msgs, w = rand_instance(31 + c + e, c, l, m)
+    pr, _ = gbgen.probes(32 + e, msgs, 40, e, l, random_count=8)
+    T = 12
+    st, it, ss = oracle.decode(w, c, l, pr, SOS, gamma=gamma, max_iters=T)
+    A = w.astype(np.int64) + gamma * np.eye(c * l, dtype=np.int64)
+    got = oracle.unpack_state(st, c, l)
+    for i, p in enumerate(pr):
+        v = np.zeros(c * l, np.int64)
+        for cc in range(c):
+            if p[cc] != ERASED:
+                v[cc * l + int(p[cc])] = 1
+        rounds, status = T, MAX_ITERS
+        for r in range(1, T + 1):
+            blk = (A @ v).reshape(c, l)
+            vn = (blk == blk.max(axis=1, keepdims=True)).astype(np.int64).reshape(-1)
+            done = np.array_equal(vn, v)
+            v = vn
+            if done:
+                rounds, status = r, CONVERGED
+                break
+        assert (int(it[i]), int(ss[i])) == (rounds, status), f"probe {i}"
+        np.testing.assert_array_equal(got[i], v, err_msg=f"probe {i}")
+
+
 def test_fixed_points_and_closed_cases_all_rules():
     """Lemma 2 (L541-548) and closed cases of SURVEY §8c:
     * stored message, e=0, gamma>=1: SOS/SOM 1 round unchanged, hybrid 0;
