@@ -22,6 +22,11 @@ Parity status per function (DESIGN.md §"Oracle pins"):
                PAPER.md L668-669 pool example.
   decode HYB   pinned: F2 (== SOM on clique-consistent probes), F3 prune
                identity, brute-force frozen-known fixed point, e=0 / e=C.
+  work counter pinned (``with_blocks=True``): equals an independent
+               walk-by-walk replay of PAPER.md L445-451 (tests/brute.py
+               decode_work) on random tiny instances, and the closed forms
+               for M=0 and a single stored clique (SOM, hybrid); SOS counts
+               rounds.
 """
 from __future__ import annotations
 

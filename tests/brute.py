@@ -114,3 +114,65 @@ def consistent_cliques(msgs, probe, erased=0xFFFF):
         if all(p == erased or p == mm for p, mm in zip(probe, m)):
             out.append(m)
     return out
+
+
+# ---------------------------------------------------------------- work counter
+def walk_blocks(w, c, l, v, i, scope):
+    """L-bit blocks thread i examines in one bail-out-early walk (PAPER.md
+    L445-451): clusters in ``scope`` other than c(i), ascending; the cluster
+    that contributes no signal is examined and stops the walk.  Returns
+    (blocks, survived)."""
+    ci = i // l
+    blocks = 0
+    for cc in range(c):
+        if cc == ci or cc not in scope:
+            continue
+        blocks += 1
+        if not has_support(w, c, l, v, i, cc):
+            return blocks, False
+    return blocks, True
+
+
+def decode_work(w, c, l, probe, rule, max_iters=200, erased=0xFFFF):
+    """Blocks read by a whole SOM (rule 1) or hybrid (rule 2) decode, walk by
+    walk: every round, every active in-scope neuron walks (SOM: all clusters;
+    hybrid: the erased clusters, Alg. 2, with the (C-e)*e blocks of
+    the known rows its prune reads, Alg. 2).  The next state is read
+    off the walks themselves (a neuron stays iff its walk completes), so this
+    shares nothing with the oracle's Eq.(6)-(7) sum.  Returns (blocks, rounds)."""
+    probe = list(probe)
+    known = [cc for cc in range(c) if probe[cc] != erased]
+    er = [cc for cc in range(c) if probe[cc] == erased]
+    v = np.zeros(c * l, np.uint8)
+    for cc in known:
+        if probe[cc] >= l:
+            return 0, 0
+        v[cc * l + probe[cc]] = 1
+    blocks = 0
+    if rule == 1:
+        for cc in er:
+            v[cc * l:(cc + 1) * l] = 1
+        scope, movable = set(range(c)), set(range(c))
+    else:
+        if not er:
+            return 0, 0
+        for cc in er:
+            col = np.ones(l, np.uint8)
+            for k in known:
+                col &= w[k * l + probe[k], cc * l:(cc + 1) * l]
+            v[cc * l:(cc + 1) * l] = col
+        blocks += len(known) * len(er)
+        scope, movable = set(er), set(er)
+    for r in range(1, max_iters + 1):
+        vn = v.copy()
+        for i in np.flatnonzero(v):
+            if i // l not in movable:
+                continue
+            b, ok = walk_blocks(w, c, l, v, i, scope)
+            blocks += b
+            if not ok:
+                vn[i] = 0
+        if (vn == v).all():
+            return blocks, r
+        v = vn
+    return blocks, max_iters

@@ -520,3 +520,53 @@ def test_scenario1_rate_bands():
     assert r[(6, SOM)] >= 0.17 and r[(6, SOM)] > r[(6, SOS)]
     for e in (3, 5, 6):
         np.testing.assert_array_equal(rates[(e, SOM)], rates[(e, HYBRID)])
+
+
+# ---------------------------------------------------------------- work counter (§8c / §8d)
+def test_work_counter_equals_bruteforce_walks():
+    """The oracle's bail-out work counter (``with_blocks=True``; SURVEY §8c
+    "Work counters") equals the blocks examined by an independent walk-by-walk
+    replay of PAPER.md L445-451 (tests/brute.py ``decode_work``): SOM walks
+    every cluster for every active neuron, hybrid walks the erased clusters
+    and adds the (C-e)*e known-row blocks of its prune (Alg. 2).
+    The replay's next state comes from the walks themselves (a neuron stays
+    iff its walk completes), so it also re-checks the rounds.  SOS counts
+    rounds (one dense product each, Eq.(11))."""
+    n = 0
+    for c, l, msgs, w, pr, e in _tiny_cases(400, 11):
+        for rule in (SOM, HYBRID):
+            st, it, ss, blk = oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=200, with_blocks=True)
+            b, r = brute.decode_work(w, c, l, pr[0], rule)
+            assert blk[0] == b and it[0] == r, (c, l, e, rule, blk[0], b, it[0], r)
+            n += 1
+        st, it, ss, blk = oracle.decode(w, c, l, pr, SOS, gamma=1, max_iters=9, with_blocks=True)
+        assert blk[0] == it[0]
+    assert n == 800
+
+
+@pytest.mark.parametrize("c,l", [(8, 128), (5, 7)])
+def test_work_counter_closed_forms(c, l):
+    """Closed forms of the bail-out-early walk count:
+    * M=0, 0<e<C: SOM round 1 walks each of the (C-e) + e*L active neurons one
+      block (the first other cluster is silent, W=0), round 2 finds nothing
+      active -> C-e+e*L blocks, 2 rounds; hybrid reads only its prune (C-e)*e;
+    * one stored clique, 1<=e<=C: SOM round 1 = C(C-1) (clique neurons walk
+      every other cluster) + e(L-1) (a non-clique erased neuron has no edge,
+      one block), round 2 = C(C-1) -> 2C(C-1)+e(L-1); e=0 -> C(C-1), 1 round;
+      hybrid (1<=e<C): prune (C-e)e + e clique neurons walking the e-1 other
+      erased clusters = e(C-1)."""
+    one = gbgen.messages(5, 1, c, l)
+    w1, _ = oracle.store(one, c, l)
+    w0 = np.zeros_like(w1)
+    for e in range(0, c + 1):
+        pr, _ = gbgen.probes(e + 1, one, 3, e, l)
+        _, it, _, blk = oracle.decode(w1, c, l, pr, SOM, gamma=1, with_blocks=True)
+        want = c * (c - 1) if e == 0 else 2 * c * (c - 1) + e * (l - 1)
+        assert (blk == want).all(), (e, blk, want)
+        if 1 <= e < c:
+            _, it, _, blk = oracle.decode(w1, c, l, pr, HYBRID, gamma=1, with_blocks=True)
+            assert (blk == e * (c - 1)).all() and (it == 1).all()
+            _, it, _, blk = oracle.decode(w0, c, l, pr, SOM, gamma=1, with_blocks=True)
+            assert (blk == c - e + e * l).all() and (it == 2).all()
+            _, it, _, blk = oracle.decode(w0, c, l, pr, HYBRID, gamma=1, with_blocks=True)
+            assert (blk == (c - e) * e).all() and (it == 1).all()
