@@ -6,9 +6,10 @@ Driver contract (one JSON line from rank 0):
   torchrun --nproc-per-node N bench.py --gpus N ...     (N > 1, NCCL)
 
 A step is one pass of the whole hot path over one batch:
-  gb_clear -> gb_store(this rank's shard of the M messages) -> [N>1: NCCL
-  all-reduce MAX of W8 (uint8)] -> gb_seal -> gb_decode(hybrid, this rank's
-  K probes, device-resident).  Weak scaling: K probes per GPU.
+  rank 0: gb_clear -> gb_store(the M messages) -> gb_seal; [N>1: NCCL broadcast
+  of rank 0's packed rows Wb; other ranks: gb_clear -> gb_or_bits -> gb_seal]
+  -> gb_decode(hybrid, this rank's K probes, device-resident).  Weak scaling:
+  K probes per GPU.
 Default workload = BASELINE config C3: c=8 l=128, M=20000, e=4 erased of 8,
 hybrid rule, gamma=2, max_iters=20, K=10^7 probes per GPU.
 
@@ -163,9 +164,11 @@ class ClockSampler:
                                                           if r[1][3].replace(".", "").isdigit()), default=None)}
 
 
-def cpu_oracle_sample(msgs, probes, c, l, rule, gamma, max_iters, budget_s, gpu_out=None, idx0=0):
-    """Time the CPU oracle (as it stands) on a bounded prefix of the workload."""
-    os.environ["OMP_NUM_THREADS"] = str(host_cores())   # all host cores (torchrun sets 1)
+def cpu_oracle_sample(msgs, probes, c, l, rule, gamma, max_iters, budget_s, gpu_out=None, threads=None):
+    """Time the CPU oracle (as it stands) on a bounded prefix of the workload.  Returns
+    (n, seconds, parity of the prefix vs the GPU, mean bail-out blocks per probe) -- the
+    blocks are the oracle's work counter (PAPER.md L445-451 walk; SOS: rounds)."""
+    os.environ["OMP_NUM_THREADS"] = str(threads or host_cores())   # all host cores (torchrun sets 1)
     import numpy as np
     import oracle
     w, _ = oracle.store(msgs, c, l)
@@ -175,13 +178,13 @@ def cpu_oracle_sample(msgs, probes, c, l, rule, gamma, max_iters, budget_s, gpu_
     rate = cal / max(time.perf_counter() - t0, 1e-6)
     n = int(min(len(probes), max(cal, rate * budget_s)))
     t0 = time.perf_counter()
-    st, it, ss = oracle.decode(w, c, l, probes[:n], rule, gamma=gamma, max_iters=max_iters)
+    st, it, ss, blk = oracle.decode(w, c, l, probes[:n], rule, gamma=gamma, max_iters=max_iters, with_blocks=True)
     dt = time.perf_counter() - t0
     parity = None
     if gpu_out is not None:
         gs, gi, gt = gpu_out
         parity = bool(np.array_equal(gs[:n], st) and np.array_equal(gi[:n], it) and np.array_equal(gt[:n], ss))
-    return n, dt, parity
+    return n, dt, parity, float(blk.mean())
 
 
 def run_reference(args, cfg):
@@ -229,14 +232,27 @@ def run_reference(args, cfg):
     return 0
 
 
+def io_bytes_per_step(c, l, k):
+    nw = c * ((l + 31) // 32)
+    return k * (2 * c + 4 * nw + 3)
+
+
+def l2_policy(c, l, k):
+    """(flush before every timed step?, the config text) -- a function of the workload only,
+    so both arms print the same config."""
+    io = io_bytes_per_step(c, l, k)
+    if io >= L2_FLUSH_BYTES // 2:
+        return False, "inputs larger than L2 (%.0f MB of probes+results per step per GPU; L2 126 MB)" % (io / 1e6)
+    return True, "L2 flushed (512 MiB write) before each timed step; per-step event windows summed"
+
+
 def config_dict(args, cfg, ws):
     c, l, m, e, rule, k, desc = cfg
     return {"workload": desc, "c": c, "l": l, "M": m, "erased": e, "rule": RULE_NAMES[rule],
             "gamma": args.gamma, "max_iters": args.max_iters, "probes_per_gpu": k,
-            "global_batch": k * ws, "parallelism": f"dp{ws} (probe shards; W merged by NCCL MAX)",
-            "l2": "inputs larger than L2 (probes 16 B + state/iters/status 131 B per probe; "
-                  "1.47 GB per step at K=10^7)",
-            "seed": SEED}
+            "global_batch": k * ws,
+            "parallelism": f"dp{ws} (probe shards; W stored on rank 0, packed rows broadcast over NCCL)",
+            "l2": l2_policy(c, l, k)[1], "seed": SEED}
 
 
 SM_COUNT, SM_CLOCK_GHZ = 148, 1.965   # B200 (B200_PROFILING.md); clocks sampled in the C3 line
@@ -280,9 +296,11 @@ def run_store(args, cfg):
     shard = torch.from_numpy(np.ascontiguousarray(msgs[lo:hi]).view(np.int16)).to(dev)
     net = gb.Net(c, l, device=local)
     stream = torch.cuda.current_stream()
-    store_step = gdist.sharded_store_bits if args.merge == "bits" else gdist.sharded_store
+    store_step = {"bits": gdist.sharded_store_bits, "max": gdist.sharded_store,
+                  "upper": gdist.sharded_store_upper}[args.merge]
     for _ in range(args.warmup):
         store_step(net, shard)
+    gdist.seal_status_all(net)
     torch.cuda.synchronize()
     l0 = net.launch_count()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -306,8 +324,10 @@ def run_store(args, cfg):
             "data": "synthetic (gbgen, seed 0x5EED)",
             "config": {"workload": desc, "c": c, "l": l, "M": m, "messages_per_gpu": hi - lo,
                        "edge_writes_per_message": c * (c - 1),
-                       "merge": ("all-gather of packed partial W + gb_or_bits" if args.merge == "bits"
-                                 else "all-reduce MAX of u8 W8") if ws > 1 else "none (1 rank)"},
+                       "merge": {"bits": "all-gather of packed partial W + gb_or_bits",
+                                 "max": "all-reduce MAX of u8 W8",
+                                 "upper": "all-gather of the packed upper-triangle blocks + gb_or_upper"}[args.merge]
+                                if ws > 1 else "none (1 rank)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
                          "traffic": None, "kernel": "store_priv_kernel+apply_kernel+seal_kernel",
                          "note": "bytes = message input + W8 + seal; the store kernel is bound on chip by "
@@ -332,13 +352,16 @@ def main():
     ap.add_argument("--messages", type=int, default=None)
     ap.add_argument("--probes", type=int, default=None)
     ap.add_argument("--gamma", type=int, default=2)
-    ap.add_argument("--merge", default="bits", choices=["bits", "max"],
-                    help="C5 store merge over ranks: packed all-gather + OR (N3) or u8 MAX all-reduce")
+    ap.add_argument("--merge", default="upper", choices=["bits", "max", "upper"],
+                    help="C5 store merge over ranks: all-gather of the packed upper triangle + OR (N3), "
+                         "of the whole packed W + OR, or u8 MAX all-reduce")
     ap.add_argument("--max-iters", type=int, default=20)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=18.0)   # calibration on 256 probes overestimates the time (~0.7x measured)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=None,
+                    help="host threads of the cpu_baseline oracle (default: all cores; 1 for the C1 figure)")
     args = ap.parse_args()
     c, l, m, e, rule, k, desc = CONFIGS[args.config]
     if args.rule is not None:
@@ -373,18 +396,20 @@ def main():
 
     msgs = gbgen.messages(SEED, m, c, l)
     probes, _ = gbgen.probes(SEED + 1, msgs, k, e, l, start=gdist.weak_bounds(k, rank)[0])
-    my_msgs = np.ascontiguousarray(gdist.message_shard(msgs, rank, ws))
-    msgs_d = torch.from_numpy(my_msgs.view(np.int16)).to(dev)
+    # W is stored on rank 0 and replicated (north_star): only rank 0 holds the messages
+    my_msgs = msgs if rank == 0 else msgs[:0]
+    msgs_d = torch.from_numpy(np.ascontiguousarray(my_msgs).view(np.int16)).to(dev)
     probes_d = torch.from_numpy(probes.view(np.int16)).to(dev)
     net = gb.Net(c, l, device=local)
     out = net.alloc_outputs(k, device=True)
-    w8 = net.weights()
     stream = torch.cuda.current_stream()
     nw = net.nw
     t_dec = []
 
     def step(timed):
-        gdist.sharded_store(net, msgs_d)   # clear + store shard + [NCCL MAX merge] + seal
+        # rank 0: clear + store + seal; [N>1: broadcast of the packed rows; others: clear +
+        # or_bits + seal].  The seal does not synchronise the host.
+        gdist.replicated_store(net, msgs_d)
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -395,6 +420,7 @@ def main():
 
     for _ in range(args.warmup):
         step(False)
+    gdist.seal_status_all(net)   # the seals of the warm-up found W well formed (outside the timed region)
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
@@ -403,8 +429,8 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = net.launch_count()
-    io_bytes = k * (2 * c + 4 * nw + 3)
-    if io_bytes >= L2_FLUSH_BYTES // 2:
+    flush_l2, l2_note = l2_policy(c, l, k)
+    if not flush_l2:
         # inputs + outputs of one step are larger than L2: one event window over all steps
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
@@ -413,7 +439,6 @@ def main():
         ev1.record(stream)
         torch.cuda.synchronize()
         ms = ev0.elapsed_time(ev1)
-        l2_note = ("inputs larger than L2 (%.0f MB of probes+results per step per GPU; L2 126 MB)" % (io_bytes / 1e6))
     else:
         # small batch: flush L2 (write a 512 MiB buffer) before every timed step; per-step event
         # windows (excluding the flush) are summed
@@ -428,7 +453,6 @@ def main():
             wins.append((a0, a1))
         torch.cuda.synchronize()
         ms = sum(a0.elapsed_time(a1) for a0, a1 in wins)
-        l2_note = "L2 flushed (512 MiB write) before each timed step; per-step event windows summed"
     if dist is not None:
         dist.barrier()
     clocks = sampler.stop(first)
@@ -483,17 +507,19 @@ def main():
             peak_wf = torch.cuda.get_device_properties(dev).multi_processor_count * sm_clk * 1e6
             roof["onchip"] = {"resource": "shared-memory wavefronts (LSU data pipe, 1 per SM per clock)",
                               "wavefronts_per_probe": wpp, "achieved_per_s": per_s, "peak_per_s": peak_wf,
-                              "frac": per_s / peak_wf, "source": ncu_entry(kernel, args.config).get("source")}
+                              "frac": per_s / peak_wf, "source": ncu_entry(kernel, args.config).get("source"),
+                              "note": "wavefronts per probe from the committed ncu capture named in source "
+                                      "(ncu cannot run inside the timed bench); time from this run"}
 
     # e2e through the C-ABI with pinned host buffers
     e2e = None
     if not args.no_e2e:
-        msgs_h = torch.from_numpy(my_msgs.view(np.int16)).pin_memory()
+        msgs_h = torch.from_numpy(np.ascontiguousarray(my_msgs).view(np.int16)).pin_memory()
         probes_h = torch.from_numpy(probes.view(np.int16)).pin_memory()
         out_h = net.alloc_outputs(k, device=False, pin=True)
 
         def e2e_step():
-            gdist.sharded_store(net, msgs_h)
+            gdist.replicated_store(net, msgs_h)
             net.decode(probes_h, rule, gamma=args.gamma, max_iters=args.max_iters, out=out_h)
 
         e2e_step()
@@ -522,13 +548,33 @@ def main():
         gs = out[0].cpu().numpy().view(np.uint32)
         gi = out[1].cpu().numpy().view(np.uint16)
         gt = out[2].cpu().numpy()
-        n, dt, parity = cpu_oracle_sample(msgs, probes, c, l, rule, args.gamma, args.max_iters,
-                                          args.cpu_budget, (gs, gi, gt))
+        n, dt, parity, blk = cpu_oracle_sample(msgs, probes, c, l, rule, args.gamma, args.max_iters,
+                                               args.cpu_budget, (gs, gi, gt), threads=args.cpu_threads)
+        if rule != 0:
+            # algorithmic W-row bytes of the paper's bail-out-early walk (PAPER.md
+            # L445-451; hybrid: + the (C-e)e prune blocks), counted by the oracle on the sample
+            wrow = blk * l / 8.0
+            roof["wrow"] = {"blocks_per_probe": blk, "bytes_per_probe": wrow,
+                            "achieved_GBps": wrow * k / (dec_ms / 1e3) / 1e9,
+                            "source": f"oracle work counter on the cpu_baseline sample ({n} probes)",
+                            "note": "L-bit blocks of W the paper's per-neuron walk reads; the kernel's push "
+                                    "reads other rows (it ORs source rows until the target is covered)"}
         cpu = {"value": n / dt, "unit": "probes/s", "cores": int(os.environ.get("OMP_NUM_THREADS", host_cores())),
                "kind": "oracle", "sample": f"first {n} probes of the same batch ({desc}), W from the same "
                                            f"{m} messages; {dt:.1f} s", "cpu": cpu_model(),
                "parity_vs_gpu_on_sample": parity}
 
+    conv = None
+    if rank == 0:
+        # E5 (fig:converge): probes converged after each round (cumulative)
+        it_all = out[1].cpu().numpy().view(np.uint16).astype(np.int64)
+        st_all = out[2].cpu().numpy()
+        ok = st_all == 0
+        hist = np.bincount(it_all[ok], minlength=int(it_all.max(initial=0)) + 1)
+        conv = {"converged_by_round": np.cumsum(hist).tolist(), "not_converged": int((~ok).sum()),
+                "mean_rounds": float(it_all.mean()) if len(it_all) else 0.0,
+                "note": "cumulative count of probes whose status is CONVERGED with iters <= r "
+                        "(r = 0, 1, ...; hybrid counts its bail-out rounds, R6)"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "probes/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -537,8 +583,8 @@ def main():
                                                                         rule == CONFIGS[args.config][4]) else None,
                 "dtype": "u32",
                 "data": "synthetic (gbgen splitmix64, seed 0x5EED; iid uniform symbols, uniform erasures)",
-                "config": dict(config_dict(args, cfg, ws), l2=l2_note), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clocks}
+                "config": config_dict(args, cfg, ws), "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clocks, "convergence": conv}
         print(json.dumps(line), flush=True)
     net.close()
     if dist is not None:

@@ -24,10 +24,19 @@
  *    back in host memory.  Device-pointer calls are asynchronous and
  *    stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
  *  - The caller owns all input/output buffers.  The library owns W (u8 and
- *    bit-packed) and its scratch.  The scratch (work queues, overflow lists,
- *    state buffers) is per handle, so calls on one handle must be
- *    stream-ordered: issue them on one stream (or order the streams with
- *    events); use one handle per stream for concurrent decodes.
+ *    bit-packed), its sum-of-sum operands W8 + gamma*I, and a memory pool.
+ *  - Concurrency.  After gb_seal, W is
+ *    immutable and any number of host threads may call gb_decode /
+ *    gb_decode_ex on one handle at the same time, on any streams, with any
+ *    rules and gammas, provided their output buffers are distinct: every
+ *    decode allocates its scratch (work counters, overflow lists, state
+ *    scratch) stream-ordered from the handle's pool, so no two calls share a
+ *    device buffer the kernels write.  Calls that change W (gb_clear,
+ *    gb_store, gb_or_bits, gb_or_upper, gb_seal, writes through gb_weights' pointer) and
+ *    gb_set_option must not overlap decodes on the handle and must be ordered
+ *    with them (same stream, or events).  Host-buffer calls (see above) of one
+ *    handle are serialised internally.  Results do not depend on how a batch
+ *    is split over calls or streams (Eq.(11): independent columns).
  *  - Errors: functions return GB_OK (0) or a negative GB_E* code and set a
  *    thread-local message readable with gb_last_error().  No exception or
  *    abort crosses the ABI.  There is no CPU fallback: without a usable
@@ -68,6 +77,29 @@ enum {
                               state is all zero and iters is 0                  */
     GB_CYCLE = 3           /* only with GB_FLAG_CYCLE_EXIT: sum-of-sum state of
                               round r repeats round r-2 (period-2 oscillation)  */
+};
+
+/* Kernel-selection options (gb_set_option).  They choose between kernels
+ * that compute the same results (bit-exact); the defaults are the measured
+ * fastest.  No environment variable or other global state is read. */
+enum {
+    GB_OPT_SOS_PAIR = 0,       /* 1 (default): sum-of-sum on CTA pairs (cta_group::2)
+                                  where the shape allows; 0: one CTA per tile       */
+    GB_OPT_SOS_STREAMED = 1,   /* 1 (default): streamed-A sum-of-sum kernel for
+                                  1024 < n_padded <= 4096; 0: the 4-warp kernel      */
+    GB_OPT_SOM_TENSOR = 2,     /* 1: sum-of-max as exact int8 contractions on the
+                                  tensor cores (n_padded <= 1024);
+                                  0 (default): the bit-row kernels                   */
+    GB_OPT_HYB8 = 3,           /* 1 (default): the C = 8 hybrid kernel; 0: the
+                                  general shared-memory hybrid kernel               */
+    GB_OPT_L2T = 4,            /* 1 (default): thread-per-probe L2 bit kernel; 0:
+                                  warp-per-probe kernel (W rows beyond shared mem)   */
+    GB_OPT_HYB8_SPLIT = 5,     /* -1 (default): choose the C = 8 hybrid kernel's
+                                  dense-W stage split by W's density (known once a
+                                  seal's status reached the host); 0 / 1 force it   */
+    GB_OPT_STORE_SCATTER = 6   /* 1: gb_store with scattered byte writes only;
+                                  0 (default): shared-memory privatised tiles for
+                                  large batches                                      */
 };
 
 /* gb_decode_ex flags. */
@@ -113,21 +145,39 @@ int gb_clear(gb_net *net, void *stream);
  * msgs: uint16_t[m][c], row-major.  OR is idempotent and commutative, so
  * calls may come in any order and from any stream split.
  * A message holding a symbol >= l (GB_ERASED included) stores nothing and
- * is counted on the device; the count is reported by the next gb_seal.
+ * is counted on the device; the count is reported by gb_seal_status.
  * Unseals the network.  m == 0 is a no-op.  Returns GB_EINVAL for m < 0 or
  * NULL msgs with m > 0.
  */
 int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
 
 /*
+ * gb_set_option / gb_get_option -- per-handle kernel selection (GB_OPT_*).
+ * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1).  GB_EINVAL for an unknown
+ * option or value.  Not to be called while decodes on the handle run.
+ */
+int gb_set_option(gb_net *net, int option, int value);
+int gb_get_option(gb_net *net, int option, int *value);
+
+/*
  * gb_weights -- expose the library-owned u8 weight matrix W8
  * (n_padded x n_padded, row-major, W8[i][j] = w_ij in {0,1}, diagonal 0;
  * gamma is applied at decode, reading R2).  Used for NCCL
  * broadcast (replicate W) and all-reduce MAX on uint8 (merge sharded
- * stores: max over {0,1} is OR).  Writing W8 directly unseals nothing by
- * itself: call gb_seal after modifying it.  *w8 is a device pointer.
+ * stores: max over {0,1} is OR).  Handing out the writable pointer (w8 not
+ * NULL) unseals the network: decode returns GB_ESTATE until the next
+ * gb_seal, so a W8 edit can never be decoded through a stale packed copy.
+ * *w8 is a device pointer.  w8 == NULL only reports the size.
  */
 int gb_weights(gb_net *net, uint8_t **w8, int64_t *nbytes);
+
+/*
+ * gb_weights_view -- the same W8 pointer for reading only (an NCCL broadcast
+ * source, a comparison): the net stays sealed.  Writing through it is a
+ * contract violation (decode would keep using the packed copy); use
+ * gb_weights to edit W8.
+ */
+int gb_weights_view(gb_net *net, const uint8_t **w8, int64_t *nbytes);
 
 /*
  * gb_bits -- expose the library-owned packed rows Wb (n_padded x n_padded/32
@@ -152,15 +202,48 @@ int gb_bits(gb_net *net, uint32_t **wb, int64_t *nbytes);
 int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream);
 
 /*
+ * gb_pack_upper -- the upper triangle of the sealed Wb, packed: for every
+ * cluster pair a < b (lexicographic), the Lp x Wc words of Wb rows
+ * a*Lp .. a*Lp+Lp-1, words b*Wc .. b*Wc+Wc-1, row-major.  W is symmetric
+ * (PAPER.md L306), so this carries all of W in C(C-1)/2 of the C^2 blocks:
+ * the smallest form to exchange between ranks (about
+ * half of gb_bits' bytes).  *nwords (if not NULL) receives the uint32 count
+ * (Lp*Wc*C*(C-1)/2); out may be NULL to query it, else a device buffer of
+ * that many words on the handle's device.  Stream-ordered.  GB_ESTATE if not
+ * sealed.
+ */
+int gb_pack_upper(gb_net *net, uint32_t *out, int64_t *nwords, void *stream);
+
+/*
+ * gb_or_upper -- OR `count` packed upper-triangle sets (consecutive, each in
+ * gb_pack_upper's layout, device memory) into W8, both w_ij and its mirror
+ * w_ji (Eq.(1) stores both directions).  Unseals; stream-ordered; count == 0
+ * is a no-op; GB_EINVAL for count < 0 or NULL sets.
+ */
+int gb_or_upper(gb_net *net, const uint32_t *sets, int64_t count, void *stream);
+
+/*
  * gb_seal -- freeze W for retrieval ("At the retrieval stage,
  * the variables w are fixed"): pack W8 into bit rows (the B200 counterpart of
  * the compressed W' of L381 / Alg. 2 line 6) and check the structural
  * invariants w_ij = w_ji (L306) and no intra-cluster or padding edges (L145).
- * Synchronizes `stream`.  Returns GB_EINVAL if W8 breaks an invariant (the
- * net stays unsealed) or if a previous gb_store skipped messages with invalid
- * symbols (the net IS sealed in that case; the message says how many).
+ * Asynchronous and stream-ordered: one kernel, no host synchronisation.  Its
+ * last CTA publishes the outcome into pinned host memory; gb_seal_status
+ * reports it.  Decodes may be issued right away (stream-ordered after the
+ * seal); a gb_decode issued after the outcome reached the host refuses a W
+ * that broke the invariants (GB_ESTATE).
  */
 int gb_seal(gb_net *net, void *stream);
+
+/*
+ * gb_seal_status -- wait for the most recent gb_seal and report its outcome:
+ * GB_OK; GB_EINVAL if W8 breaks an invariant (the net is then unsealed) or if
+ * gb_store calls between the previous seal (or gb_clear) and this one skipped
+ * messages with invalid symbols (the net IS sealed; the message says how
+ * many); GB_ESTATE if no seal was issued.  Blocks the calling thread only;
+ * repeated calls report the same seal's outcome until the next gb_seal.
+ */
+int gb_seal_status(gb_net *net);
 
 /*
  * gb_decode -- retrieve k probes in one batch (Eq.(11)

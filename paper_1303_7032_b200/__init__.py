@@ -29,9 +29,14 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB: experiment builds
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
-EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_weights", "gb_bits", "gb_or_bits", "gb_seal",
-           "gb_decode", "gb_decode_ex", "gb_info", "gb_launch_count", "gb_decode_kernel", "gb_last_error",
-           "gb_version")
+EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_set_option", "gb_get_option", "gb_weights",
+           "gb_weights_view", "gb_bits", "gb_or_bits", "gb_pack_upper", "gb_or_upper", "gb_seal", "gb_seal_status",
+           "gb_decode", "gb_decode_ex", "gb_info",
+           "gb_launch_count", "gb_decode_kernel", "gb_last_error", "gb_version")
+
+# gb_set_option keys (include/gb.h GB_OPT_*): kernel choices with identical results
+OPTIONS = {"sos_pair": 0, "sos_streamed": 1, "som_tensor": 2, "hyb8": 3, "l2t": 4, "hyb8_split": 5,
+           "store_scatter": 6}
 
 _lib = None
 
@@ -58,9 +63,15 @@ def lib() -> ctypes.CDLL:
         "gb_clear": ([P, P], i32),
         "gb_store": ([P, P, i64, P], i32),
         "gb_weights": ([P, PP, ctypes.POINTER(i64)], i32),
+        "gb_weights_view": ([P, PP, ctypes.POINTER(i64)], i32),
         "gb_seal": ([P, P], i32),
+        "gb_seal_status": ([P], i32),
+        "gb_set_option": ([P, i32, i32], i32),
+        "gb_get_option": ([P, i32, ctypes.POINTER(i32)], i32),
         "gb_bits": ([P, PP, ctypes.POINTER(i64)], i32),
         "gb_or_bits": ([P, P, i64, P], i32),
+        "gb_pack_upper": ([P, P, ctypes.POINTER(i64), P], i32),
+        "gb_or_upper": ([P, P, i64, P], i32),
         "gb_decode": ([P, P, i64, i32, i32, i32, P, P, P, P], i32),
         "gb_decode_ex": ([P, P, i64, i32, i32, i32, ctypes.c_uint, P, P, P, P], i32),
         "gb_info": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
@@ -71,6 +82,8 @@ def lib() -> ctypes.CDLL:
         "gb_version": ([], ctypes.c_char_p),
     }
     for name, (args, res) in sig.items():
+        if "GB_LIB" in os.environ and not hasattr(L, name):
+            continue   # an older experiment build (tools/ab.sh) without a newer entry point
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
@@ -111,9 +124,12 @@ class _CudaArray:
 
 
 class Net:
-    """One GBNN network on one CUDA device (gb_net handle)."""
+    """One GBNN network on one CUDA device (gb_net handle).
 
-    def __init__(self, c: int, l: int, device: int = 0):
+    ``options``: kernel-selection options (``OPTIONS`` keys -> 0/1, ``hyb8_split``
+    also -1), passed to gb_set_option; they pick between bit-exact kernels."""
+
+    def __init__(self, c: int, l: int, device: int = 0, **options):
         h = ctypes.c_void_p()
         _check(lib().gb_create(c, l, device, ctypes.byref(h)))
         self._h = h
@@ -121,6 +137,16 @@ class Net:
         self.wc = (l + 31) // 32
         self.n_padded = c * 32 * self.wc
         self.nw = c * self.wc
+        for k, v in options.items():
+            self.set_option(k, v)
+
+    def set_option(self, name, value: int):
+        _check(lib().gb_set_option(self._h, OPTIONS[name] if isinstance(name, str) else int(name), int(value)))
+
+    def option(self, name) -> int:
+        v = ctypes.c_int()
+        _check(lib().gb_get_option(self._h, OPTIONS[name] if isinstance(name, str) else int(name), ctypes.byref(v)))
+        return v.value
 
     def close(self):
         if getattr(self, "_h", None):
@@ -141,15 +167,32 @@ class Net:
         assert msgs.ndim == 2 and msgs.shape[1] == self.c
         _check(lib().gb_store(self._h, ctypes.c_void_p(_addr(msgs)), m, _stream(stream)))
 
-    def seal(self, stream=None):
+    def seal(self, stream=None, check: bool = True):
+        """gb_seal (asynchronous); with ``check`` also gb_seal_status (waits for it and
+        raises GBError on broken invariants or skipped invalid messages)."""
         _check(lib().gb_seal(self._h, _stream(stream)))
+        if check:
+            self.seal_status()
+
+    def seal_status(self):
+        _check(lib().gb_seal_status(self._h))
 
     def weights(self):
-        """The library-owned W8 as a torch uint8 cuda tensor [n_p, n_p] (no copy)."""
+        """The library-owned W8 as a torch uint8 cuda tensor [n_p, n_p] (no copy).
+        Unseals the net (it may be written): call seal() before decoding."""
         import torch
         p = ctypes.c_void_p()
         nb = ctypes.c_int64()
         _check(lib().gb_weights(self._h, ctypes.byref(p), ctypes.byref(nb)))
+        arr = _CudaArray(p.value, (self.n_padded, self.n_padded), "|u1")
+        return torch.as_tensor(arr, device=f"cuda:{self.device}")
+
+    def weights_view(self):
+        """W8 for reading only (gb_weights_view): the net stays sealed; do not write it."""
+        import torch
+        p = ctypes.c_void_p()
+        nb = ctypes.c_int64()
+        _check(lib().gb_weights_view(self._h, ctypes.byref(p), ctypes.byref(nb)))
         arr = _CudaArray(p.value, (self.n_padded, self.n_padded), "|u1")
         return torch.as_tensor(arr, device=f"cuda:{self.device}")
 
@@ -168,6 +211,27 @@ class Net:
         assert bits.is_cuda and bits.is_contiguous() and tuple(bits.shape[-2:]) == (self.n_padded, self.nw)
         count = bits.numel() // (self.n_padded * self.nw)
         _check(lib().gb_or_bits(self._h, ctypes.c_void_p(bits.data_ptr()), count, _stream(stream)))
+
+    def upper_words(self) -> int:
+        n = ctypes.c_int64()
+        _check(lib().gb_pack_upper(self._h, None, ctypes.byref(n), None))
+        return n.value
+
+    def pack_upper(self, out=None, stream=None):
+        """gb_pack_upper: the upper-triangle blocks of the sealed Wb as an int32 cuda tensor."""
+        import torch
+        n = self.upper_words()
+        if out is None:
+            out = torch.empty((n,), dtype=torch.int32, device=f"cuda:{self.device}")
+        assert out.is_cuda and out.is_contiguous() and out.numel() == n
+        _check(lib().gb_pack_upper(self._h, ctypes.c_void_p(out.data_ptr()), None, _stream(stream)))
+        return out
+
+    def or_upper(self, sets, stream=None):
+        """gb_or_upper: OR packed upper-triangle sets ([count, n] int32 cuda tensor) into W8."""
+        n = self.upper_words()
+        assert sets.is_cuda and sets.is_contiguous() and sets.numel() % n == 0
+        _check(lib().gb_or_upper(self._h, ctypes.c_void_p(sets.data_ptr()), sets.numel() // n, _stream(stream)))
 
     def info(self):
         c, l, n, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int64()

@@ -8,16 +8,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <new>
 
 #include "gb_internal.h"
-
-namespace gb {
-cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                               uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
-cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k, int rule,
-                                  int gamma, int max_iters, int cyc, uint32_t *state, uint16_t *iters,
-                                  uint8_t *status, cudaStream_t st);
-}
 
 namespace {
 
@@ -68,16 +61,55 @@ int where(const void *p, int dev) {
     return 0;
 }
 
-int ensure_stage(gb_net *net, size_t bytes) {
-    if (net->stage_bytes >= bytes) return GB_OK;
-    if (net->stage) cudaFree(net->stage);
-    net->stage = nullptr;
-    net->stage_bytes = 0;
-    if (cudaMalloc(&net->stage, bytes) != cudaSuccess) {
-        cudaGetLastError();
-        return fail(GB_ENOMEM, "staging buffer of %zu bytes", bytes);
+// Resolve the outcome of the most recent gb_seal (its status is published by the seal
+// kernel into mapped pinned memory).  block = false: only if the seal has completed.
+// Returns GB_OK, GB_EINVAL (broken invariants or skipped messages; message set) or
+// 1 = still running (block = false).
+int resolve_seal(gb_net *net, bool block) {
+    std::lock_guard<std::mutex> lk(net->smu);
+    if (net->seal_gen == 0) return fail(GB_ESTATE, "gb_seal_status: no seal issued");
+    if (net->seal_resolved != net->seal_gen) {
+        if (block) {
+            cudaError_t e = cudaEventSynchronize(net->seal_event);
+            if (e != cudaSuccess) return cuda_fail(e, "gb_seal_status: sync");
+        } else {
+            const cudaError_t q = cudaEventQuery(net->seal_event);
+            if (q == cudaErrorNotReady) return 1;
+            if (q != cudaSuccess) return cuda_fail(q, "gb_seal_status: query");
+        }
+        const volatile gb::Status *h = net->hstat;
+        if (h->gen != net->seal_gen) return fail(GB_ECUDA, "gb_seal_status: status of seal %llu not published",
+                                                 (unsigned long long)net->seal_gen);
+        const unsigned flag = h->flags;
+        const unsigned long long inv = h->invalid;
+        const double pairs = (double)net->s.C * (net->s.C - 1) * (double)net->s.L * net->s.L;
+        net->density.store(pairs > 0 ? h->edges / pairs : 0.0);
+        if (net->seal_epoch != net->reported_epoch) {   // gb_clear reset the device count
+            net->reported_epoch = net->seal_epoch;
+            net->invalid_reported = 0;
+        }
+        const unsigned long long fresh = inv - net->invalid_reported;
+        net->invalid_reported = inv;
+        net->seal_resolved = net->seal_gen;
+        const unsigned structural = flag & ~gb::kFlagStoreInvalid;
+        net->seal_broken = structural != 0;
+        net->seal_rc = GB_OK;
+        net->seal_msg[0] = 0;
+        if (structural) {
+            net->sealed = false;
+            net->seal_rc = GB_EINVAL;
+            snprintf(net->seal_msg, sizeof net->seal_msg, "gb_seal: W8 breaks Eq.(1) invariants:%s%s%s%s",
+                     (structural & gb::kFlagNotBinary) ? " non-binary entry" : "",
+                     (structural & gb::kFlagAsym) ? " asymmetric" : "",
+                     (structural & gb::kFlagIntra) ? " intra-cluster edge" : "",
+                     (structural & gb::kFlagPad) ? " padding edge" : "");
+        } else if (fresh) {
+            net->seal_rc = GB_EINVAL;
+            snprintf(net->seal_msg, sizeof net->seal_msg,
+                     "gb_seal: %llu stored message(s) had a symbol >= L and were skipped", fresh);
+        }
     }
-    net->stage_bytes = bytes;
+    if (net->seal_rc != GB_OK) return fail(net->seal_rc, "%s", net->seal_msg);
     return GB_OK;
 }
 
@@ -87,7 +119,7 @@ extern "C" {
 
 const char *gb_last_error(void) { return g_err; }
 
-const char *gb_version(void) { return "libgb 0.1 (sm_100a)"; }
+const char *gb_version(void) { return "libgb 0.2 (sm_100a)"; }
 
 int gb_create(int c, int l, int device, gb_net **out) {
     if (!out) return fail(GB_EINVAL, "gb_create: out is NULL");
@@ -113,34 +145,53 @@ int gb_create(int c, int l, int device, gb_net **out) {
                     device, prop.major, prop.minor);
     DeviceGuard g(device);
     if (!g.ok) return fail(GB_ECUDA, "gb_create: cudaSetDevice(%d) failed", device);
-    gb_net *net = (gb_net *)calloc(1, sizeof(gb_net));
+    gb_net *net = new (std::nothrow) gb_net();
     if (!net) return fail(GB_ENOMEM, "gb_create: host allocation");
     net->s = s;
     net->device = device;
     net->sm_count = prop.multiProcessorCount;
+    for (int o = 0; o < gb::kNumOptions; ++o) net->opt[o].store(gb::option_default(o));
     const size_t w8b = (size_t)s.np * s.np, wbb = (size_t)s.np * s.nw * sizeof(uint32_t);
+    void *hs = nullptr;
     if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb) != cudaSuccess ||
-        cudaMalloc(&net->dcount, 16) != cudaSuccess ||   // [0, 8) invalid-message count, [8, 12) flags
-        cudaMallocHost(&net->hstat, 16) != cudaSuccess ||
-        cudaMalloc(&net->queue, sizeof(unsigned long long)) != cudaSuccess ||
-        cudaMalloc(&net->ovf_count, sizeof(unsigned long long)) != cudaSuccess) {
+        cudaMalloc(&net->dcount, 32) != cudaSuccess ||
+        cudaHostAlloc(&hs, sizeof(gb::Status), cudaHostAllocMapped) != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(net->w8); cudaFree(net->wb); cudaFree(net->dcount); cudaFreeHost(net->hstat); cudaFree(net->queue); cudaFree(net->ovf_count);
-        free(net);
+        cudaFree(net->w8);
+        cudaFree(net->wb);
+        cudaFree(net->dcount);
+        if (hs) cudaFreeHost(hs);
+        delete net;
         return fail(GB_ENOMEM, "gb_create: device allocation of W (%zu bytes)", w8b + wbb);
     }
+    net->hstat = static_cast<gb::Status *>(hs);
+    memset(hs, 0, sizeof(gb::Status));
+    void *hd = nullptr;
+    cudaError_t e = cudaHostGetDevicePointer(&hd, hs, 0);
+    net->hstat_dev = static_cast<gb::Status *>(hd);
     cudaMemset(net->w8, 0, w8b);
     cudaMemset(net->wb, 0, wbb);
     net->dflag = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(net->dcount) + 8);
-    cudaMemset(net->dcount, 0, 16);
+    cudaMemset(net->dcount, 0, 32);
     for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&net->stage_stream[i], cudaStreamNonBlocking);
-    for (int i = 0; i < 4; ++i) cudaEventCreateWithFlags(&net->stage_event[i], cudaEventDisableTiming);
-    cudaError_t e = cudaDeviceSynchronize();
+    cudaEventCreateWithFlags(&net->stage_event, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&net->seal_event, cudaEventDisableTiming);
+    // per-call scratch comes from this pool (stream-ordered); keep freed blocks for reuse
+    cudaMemPoolProps pp = {};
+    pp.allocType = cudaMemAllocationTypePinned;
+    pp.location.type = cudaMemLocationTypeDevice;
+    pp.location.id = device;
+    if (e == cudaSuccess) e = cudaMemPoolCreate(&net->pool, &pp);
+    if (e == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        e = cudaMemPoolSetAttribute(net->pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) {
         gb_destroy(net);
         return cuda_fail(e, "gb_create: init");
     }
-    gb::sos_tc_make_map(net);   // TMA descriptor of W8 for the tensor-core SOS kernel
+    gb::sos_tc_make_map(net);   // TMA descriptor of W8 for the 4-warp tensor-core SOS kernel
     *out = net;
     return GB_OK;
 }
@@ -149,22 +200,38 @@ int gb_destroy(gb_net *net) {
     if (!net) return GB_OK;
     DeviceGuard g(net->device);
     cudaDeviceSynchronize();
-    for (int i = 0; i < 2; ++i) if (net->stage_stream[i]) cudaStreamDestroy(net->stage_stream[i]);
-    for (int i = 0; i < 4; ++i) if (net->stage_event[i]) cudaEventDestroy(net->stage_event[i]);
-    cudaFree(net->stage);
-    cudaFree(net->w8g);
-    cudaFree(net->vscratch);
+    for (int i = 0; i < 2; ++i)
+        if (net->stage_stream[i]) cudaStreamDestroy(net->stage_stream[i]);
+    if (net->stage_event) cudaEventDestroy(net->stage_event);
+    if (net->seal_event) cudaEventDestroy(net->seal_event);
+    for (auto &v : net->gvar) {
+        cudaFree(v.w8g);
+        if (v.ready) cudaEventDestroy(v.ready);
+    }
+    if (net->pool) cudaMemPoolDestroy(net->pool);
     cudaFree(net->w8);
     cudaFree(net->wb);
     cudaFree(net->dcount);   // also holds dflag
-    cudaFreeHost(net->hstat);
-    cudaFree(net->queue);
-    cudaFree(net->ovf);
-    cudaFree(net->ovf_count);
-    cudaFree(net->spart);
-    cudaFree(net->xscratch);
-    cudaFree(net->w4);
-    free(net);
+    if (net->hstat) cudaFreeHost(net->hstat);
+    delete net;
+    return GB_OK;
+}
+
+int gb_set_option(gb_net *net, int option, int value) {
+    if (!net) return fail(GB_EINVAL, "gb_set_option: net is NULL");
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_STORE_SCATTER)
+        return fail(GB_EINVAL, "gb_set_option: unknown option %d", option);
+    const int lo = option == GB_OPT_HYB8_SPLIT ? -1 : 0;
+    if (value < lo || value > 1) return fail(GB_EINVAL, "gb_set_option: value %d outside [%d, 1]", value, lo);
+    net->opt[option].store(value);
+    return GB_OK;
+}
+
+int gb_get_option(gb_net *net, int option, int *value) {
+    if (!net || !value) return fail(GB_EINVAL, "gb_get_option: NULL argument");
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_STORE_SCATTER)
+        return fail(GB_EINVAL, "gb_get_option: unknown option %d", option);
+    *value = net->opt[option].load();
     return GB_OK;
 }
 
@@ -173,9 +240,10 @@ int gb_clear(gb_net *net, void *stream) {
     DeviceGuard g(net->device);
     cudaStream_t st = (cudaStream_t)stream;
     GB_CUDA(cudaMemsetAsync(net->w8, 0, (size_t)net->s.np * net->s.np, st), "gb_clear");
-    GB_CUDA(cudaMemsetAsync(net->dcount, 0, 16, st), "gb_clear");   // count + flags
+    GB_CUDA(cudaMemsetAsync(net->dcount, 0, 8, st), "gb_clear");   // invalid-message count
     net->stored = 0;
     net->sealed = false;
+    net->clear_epoch += 1;
     return GB_OK;
 }
 
@@ -191,19 +259,24 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream) {
     net->sealed = false;
     net->stored += m;
     if (loc == 1) {
-        GB_CUDA(gb::launch_store(net, msgs, m, st), "gb_store: launch");
+        gb::Call cl(net, st);
+        GB_CUDA(gb::launch_store(cl, msgs, m), "gb_store: launch");
         return GB_OK;
     }
-    // Host messages: stage in chunks through device scratch (blocking).
+    // Host messages: stage in chunks through call-private device memory (blocking).
+    std::lock_guard<std::mutex> lk(net->stage_mu);
     const int64_t chunk = std::min<int64_t>(m, 1 << 20);
     const size_t row = (size_t)net->s.C * sizeof(uint16_t);
-    int rc = ensure_stage(net, (size_t)chunk * row);
-    if (rc) return rc;
-    for (int64_t s0 = 0; s0 < m; s0 += chunk) {
-        const int64_t n = std::min(chunk, m - s0);
-        GB_CUDA(cudaMemcpyAsync(net->stage, msgs + s0 * net->s.C, (size_t)n * row,
-                                cudaMemcpyHostToDevice, st), "gb_store: H2D");
-        GB_CUDA(gb::launch_store(net, (const uint16_t *)net->stage, n, st), "gb_store: launch");
+    {
+        gb::Call cl(net, st);
+        uint16_t *stage = cl.alloc_n<uint16_t>((size_t)chunk * net->s.C);
+        if (!stage) return fail(GB_ENOMEM, "gb_store: staging buffer of %zu bytes", (size_t)chunk * row);
+        for (int64_t s0 = 0; s0 < m; s0 += chunk) {
+            const int64_t n = std::min(chunk, m - s0);
+            GB_CUDA(cudaMemcpyAsync(stage, msgs + s0 * net->s.C, (size_t)n * row, cudaMemcpyHostToDevice, st),
+                    "gb_store: H2D");
+            GB_CUDA(gb::launch_store(cl, stage, n), "gb_store: launch");
+        }
     }
     GB_CUDA(cudaStreamSynchronize(st), "gb_store: sync");
     return GB_OK;
@@ -211,6 +284,16 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream) {
 
 int gb_weights(gb_net *net, uint8_t **w8, int64_t *nbytes) {
     if (!net) return fail(GB_EINVAL, "gb_weights: net is NULL");
+    if (w8) {
+        *w8 = net->w8;
+        net->sealed = false;   // a writable W8 is out: decode needs a new gb_seal
+    }
+    if (nbytes) *nbytes = (int64_t)net->s.np * net->s.np;
+    return GB_OK;
+}
+
+int gb_weights_view(gb_net *net, const uint8_t **w8, int64_t *nbytes) {
+    if (!net) return fail(GB_EINVAL, "gb_weights_view: net is NULL");
     if (w8) *w8 = net->w8;
     if (nbytes) *nbytes = (int64_t)net->s.np * net->s.np;
     return GB_OK;
@@ -230,9 +313,38 @@ int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream) {
     if (count == 0) return GB_OK;
     if (!bits) return fail(GB_EINVAL, "gb_or_bits: bits is NULL");
     DeviceGuard g(net->device);
-    if (where(bits, net->device) != 1) return fail(GB_EINVAL, "gb_or_bits: bits must be device memory of the handle's device");
+    if (where(bits, net->device) != 1)
+        return fail(GB_EINVAL, "gb_or_bits: bits must be device memory of the handle's device");
     net->sealed = false;
-    GB_CUDA(gb::launch_or_bits(net, bits, count, (cudaStream_t)stream), "gb_or_bits: launch");
+    gb::Call cl(net, (cudaStream_t)stream);
+    GB_CUDA(gb::launch_or_bits(cl, bits, count), "gb_or_bits: launch");
+    return GB_OK;
+}
+
+int gb_pack_upper(gb_net *net, uint32_t *out, int64_t *nwords, void *stream) {
+    if (!net) return fail(GB_EINVAL, "gb_pack_upper: net is NULL");
+    if (nwords) *nwords = gb::upper_words(net->s);
+    if (!out) return GB_OK;
+    if (!net->sealed) return fail(GB_ESTATE, "gb_pack_upper: network not sealed (Wb is built by gb_seal)");
+    DeviceGuard g(net->device);
+    if (where(out, net->device) != 1)
+        return fail(GB_EINVAL, "gb_pack_upper: out must be device memory of the handle's device");
+    gb::Call cl(net, (cudaStream_t)stream);
+    GB_CUDA(gb::launch_pack_upper(cl, out), "gb_pack_upper: launch");
+    return GB_OK;
+}
+
+int gb_or_upper(gb_net *net, const uint32_t *sets, int64_t count, void *stream) {
+    if (!net) return fail(GB_EINVAL, "gb_or_upper: net is NULL");
+    if (count < 0) return fail(GB_EINVAL, "gb_or_upper: count = %lld < 0", (long long)count);
+    if (count == 0) return GB_OK;
+    if (!sets) return fail(GB_EINVAL, "gb_or_upper: sets is NULL");
+    DeviceGuard g(net->device);
+    if (where(sets, net->device) != 1)
+        return fail(GB_EINVAL, "gb_or_upper: sets must be device memory of the handle's device");
+    net->sealed = false;
+    gb::Call cl(net, (cudaStream_t)stream);
+    GB_CUDA(gb::launch_or_upper(cl, sets, count), "gb_or_upper: launch");
     return GB_OK;
 }
 
@@ -240,36 +352,21 @@ int gb_seal(gb_net *net, void *stream) {
     if (!net) return fail(GB_EINVAL, "gb_seal: net is NULL");
     DeviceGuard g(net->device);
     cudaStream_t st = (cudaStream_t)stream;
-    GB_CUDA(gb::launch_seal(net, st), "gb_seal: launch");
-    net->launches += 1;
-    unsigned flag = 0;
-    unsigned long long cnt = 0;
-    // count and flags in one 16-byte copy to pinned memory, then one reset
-    GB_CUDA(cudaMemcpyAsync(net->hstat, net->dcount, 16, cudaMemcpyDeviceToHost, st), "gb_seal: status");
-    GB_CUDA(cudaStreamSynchronize(st), "gb_seal: sync");
-    memcpy(&cnt, net->hstat, sizeof cnt);
-    memcpy(&flag, reinterpret_cast<const char *>(net->hstat) + 8, sizeof flag);
-    unsigned edges = 0;
-    memcpy(&edges, reinterpret_cast<const char *>(net->hstat) + 12, sizeof edges);
     {
-        const double pairs = (double)net->s.C * (net->s.C - 1) * (double)net->s.L * net->s.L;
-        net->density = pairs > 0 ? edges / pairs : 0.0;
-    }
-    GB_CUDA(cudaMemsetAsync(net->dcount, 0, 16, st), "gb_seal: reset");
-    const unsigned structural = flag & ~gb::kFlagStoreInvalid;
-    if (structural) {
-        net->sealed = false;
-        return fail(GB_EINVAL, "gb_seal: W8 breaks Eq.(1) invariants:%s%s%s%s",
-                    (structural & gb::kFlagNotBinary) ? " non-binary entry" : "",
-                    (structural & gb::kFlagAsym) ? " asymmetric" : "",
-                    (structural & gb::kFlagIntra) ? " intra-cluster edge" : "",
-                    (structural & gb::kFlagPad) ? " padding edge" : "");
+        std::lock_guard<std::mutex> lk(net->smu);
+        net->seal_gen += 1;
+        net->seal_epoch = net->clear_epoch;
+        GB_CUDA(gb::launch_seal(net, st), "gb_seal: launch");
+        GB_CUDA(cudaEventRecord(net->seal_event, st), "gb_seal: record");
     }
     net->sealed = true;
-    net->seal_gen += 1;
-    if (cnt) return fail(GB_EINVAL, "gb_seal: %llu stored message(s) had a symbol >= L and were skipped",
-                         (unsigned long long)cnt);
     return GB_OK;
+}
+
+int gb_seal_status(gb_net *net) {
+    if (!net) return fail(GB_EINVAL, "gb_seal_status: net is NULL");
+    DeviceGuard g(net->device);
+    return resolve_seal(net, true);
 }
 
 int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
@@ -291,58 +388,74 @@ int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int g
         return fail(GB_EINVAL, "gb_decode: max_iters %d outside [1, 65535]", max_iters);
     if (k < 0) return fail(GB_EINVAL, "gb_decode: k = %lld < 0", (long long)k);
     if (!net->sealed) return fail(GB_ESTATE, "gb_decode: network not sealed (call gb_seal after gb_store)");
+    DeviceGuard g(net->device);
+    // the latest seal's outcome, if it has reached the host (no wait): a W that broke
+    // Eq.(1)'s invariants is not decoded
+    if (resolve_seal(net, false) == GB_EINVAL && net->seal_broken)
+        return fail(GB_ESTATE, "gb_decode: the last gb_seal found W8 breaking Eq.(1)'s invariants (%s)",
+                    net->seal_msg);
     if (k == 0) return GB_OK;
     if (!probes || !out_state || !out_iters || !out_status)
         return fail(GB_EINVAL, "gb_decode: NULL buffer");
-    DeviceGuard g(net->device);
     cudaStream_t st = (cudaStream_t)stream;
     const int l0 = where(probes, net->device), l1 = where(out_state, net->device),
               l2 = where(out_iters, net->device), l3 = where(out_status, net->device);
     if (l0 < 0 || l1 < 0 || l2 < 0 || l3 < 0)
         return fail(GB_EINVAL, "gb_decode: buffer on another device");
     if (l0 && l1 && l2 && l3) {
-        GB_CUDA(gb::launch_decode(net, probes, k, rule, gamma, max_iters, cyc, out_state, out_iters,
-                                  out_status, st),
+        gb::Call cl(net, st);
+        GB_CUDA(gb::launch_decode(cl, probes, k, rule, gamma, max_iters, cyc, out_state, out_iters, out_status),
                 "gb_decode: launch");
         return GB_OK;
     }
     if (l0 || l1 || l2 || l3)
         return fail(GB_EINVAL, "gb_decode: mix of host and device buffers");
 
-    // Host buffers: double-buffered pipeline over two library streams;
-    // chunk i: H2D probes -> decode -> D2H results, overlapping with chunk
-    // i+1's copies.  Ordered after `stream`'s prior work; blocks until done.
+    // Host buffers: double-buffered pipeline over the handle's two staging streams;
+    // chunk i: H2D probes -> decode -> D2H results, overlapping with chunk i+1's copies.
+    // Every chunk is its own call (private scratch).  Ordered after `stream`'s prior work;
+    // blocks until done; host-buffer calls on one handle are serialised.
+    std::lock_guard<std::mutex> lk(net->stage_mu);
     const size_t pin = (size_t)net->s.C * sizeof(uint16_t);
     const size_t pout = (size_t)net->s.nw * sizeof(uint32_t) + sizeof(uint16_t) + sizeof(uint8_t);
     const int64_t chunk = std::min<int64_t>(k, 1 << 19);
     const size_t slot = ((size_t)chunk * (pin + pout) + 255) & ~(size_t)255;
-    int rc = ensure_stage(net, 2 * slot);
-    if (rc) return rc;
-    GB_CUDA(cudaEventRecord(net->stage_event[2], st), "gb_decode: record");
+    char *stage = nullptr;
+    GB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&stage), 2 * slot, net->pool, st),
+            "gb_decode: staging buffer");
+    GB_CUDA(cudaEventRecord(net->stage_event, st), "gb_decode: record");
     for (int i = 0; i < 2; ++i)
-        GB_CUDA(cudaStreamWaitEvent(net->stage_stream[i], net->stage_event[2], 0), "gb_decode: wait");
+        GB_CUDA(cudaStreamWaitEvent(net->stage_stream[i], net->stage_event, 0), "gb_decode: wait");
     int64_t ci = 0;
-    for (int64_t s0 = 0; s0 < k; s0 += chunk, ++ci) {
+    int rc = GB_OK;
+    for (int64_t s0 = 0; s0 < k && rc == GB_OK; s0 += chunk, ++ci) {
         const int64_t n = std::min(chunk, k - s0);
         const int sl = (int)(ci & 1);
         cudaStream_t ss = net->stage_stream[sl];
-        char *base = (char *)net->stage + sl * slot;
+        char *base = stage + sl * slot;
         uint16_t *dp = (uint16_t *)base;
         uint32_t *ds = (uint32_t *)(base + (((size_t)chunk * pin + 255) & ~(size_t)255));
         uint16_t *di = (uint16_t *)((char *)ds + (size_t)chunk * net->s.nw * sizeof(uint32_t));
         uint8_t *dt = (uint8_t *)(di + chunk);
-        GB_CUDA(cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, ss),
-                "gb_decode: H2D");
-        GB_CUDA(gb::launch_decode(net, dp, n, rule, gamma, max_iters, cyc, ds, di, dt, ss), "gb_decode: launch");
-        GB_CUDA(cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, ss), "gb_decode: D2H state");
-        GB_CUDA(cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, ss),
-                "gb_decode: D2H iters");
-        GB_CUDA(cudaMemcpyAsync(out_status + s0, dt, (size_t)n, cudaMemcpyDeviceToHost, ss),
-                "gb_decode: D2H status");
+        cudaError_t e = cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, ss);
+        if (e == cudaSuccess) {
+            gb::Call cl(net, ss);
+            e = gb::launch_decode(cl, dp, n, rule, gamma, max_iters, cyc, ds, di, dt);
+        }
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
+                                cudaMemcpyDeviceToHost, ss);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, ss);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out_status + s0, dt, (size_t)n, cudaMemcpyDeviceToHost, ss);
+        if (e != cudaSuccess) rc = cuda_fail(e, "gb_decode: staged chunk");
     }
-    for (int i = 0; i < 2; ++i) GB_CUDA(cudaStreamSynchronize(net->stage_stream[i]), "gb_decode: sync");
-    return GB_OK;
+    for (int i = 0; i < 2; ++i) {
+        cudaError_t e = cudaStreamSynchronize(net->stage_stream[i]);
+        if (e != cudaSuccess && rc == GB_OK) rc = cuda_fail(e, "gb_decode: sync");
+    }
+    cudaFreeAsync(stage, st);   // both staging streams are idle now
+    return rc;
 }
 
 int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
@@ -356,23 +469,22 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
-    if (rule == GB_SUM_OF_SUM && gb::sos_fp4_enabled(net->s, 2)) return "sos_fp4_kernel";   // (gamma = 2)
+    if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net))
+        return gb::sos_tc3_pair(net) ? "sos_tc3x2_kernel" : "sos_tc3_kernel";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
-        return gb::sos_2cta_enabled(net->s) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
-    if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net->s))
-        return gb::sos_tc3_pair(net->s) ? "sos_tc3x2_kernel" : "sos_tc3_kernel";
+        return gb::sos_2cta_enabled(net) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
-    if (rule == GB_SUM_OF_MAX && gb::som_tc_enabled(net->s)) return "som_tc_kernel";
-    if (rule == GB_HYBRID && gb::decode_hyb8_supported(net->s, rule, 0, nullptr)) return "decode_hyb8_kernel";
+    if (rule == GB_SUM_OF_MAX && gb::som_tc_enabled(net)) return "som_tc_kernel";
+    if (rule == GB_HYBRID && gb::decode_hyb8_supported(net, rule, 0, nullptr)) return "decode_hyb8_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule))
-        return gb::decode_l2t_supported(net->s, rule) ? "decode_l2t_kernel" : "decode_l2_kernel";
+        return gb::decode_l2t_supported(net, rule) ? "decode_l2t_kernel" : "decode_l2_kernel";
     return "decode_generic_kernel";
 }
 
 int gb_launch_count(gb_net *net, int64_t *launches) {
     if (!net || !launches) return fail(GB_EINVAL, "gb_launch_count: NULL argument");
-    *launches = net->launches;
+    *launches = net->launches.load();
     return GB_OK;
 }
 
@@ -380,22 +492,73 @@ int gb_launch_count(gb_net *net, int64_t *launches) {
 
 namespace gb {
 
+int option_default(int o) {
+    switch (o) {
+        case kOptSosPair: return 1;
+        case kOptSosStreamed: return 1;
+        case kOptSomTensor: return 0;
+        case kOptHyb8: return 1;
+        case kOptL2t: return 1;
+        case kOptHyb8Split: return -1;
+        case kOptStoreScatter: return 0;
+        default: return 0;
+    }
+}
+
+Call::~Call() {
+    for (int i = nblk_ - 1; i >= 0; --i) cudaFreeAsync(blk_[i], st);
+}
+
+void *Call::alloc(size_t bytes) {
+    if (nblk_ == 8) {
+        err = cudaErrorMemoryAllocation;
+        return nullptr;
+    }
+    void *p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes ? bytes : 16, net->pool, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        err = cudaErrorMemoryAllocation;
+        return nullptr;
+    }
+    blk_[nblk_++] = p;
+    return p;
+}
+
+unsigned long long *Call::counters() {
+    if (!counters_) {
+        counters_ = alloc_n<unsigned long long>(2);
+        if (!counters_) return nullptr;
+        cudaError_t e = cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), st);
+        if (e != cudaSuccess) {
+            err = e;
+            counters_ = nullptr;
+        }
+    }
+    return counters_;
+}
+
+int64_t *Call::ovf(int64_t k) {
+    if (!ovf_) ovf_ = alloc_n<int64_t>((size_t)(k > 0 ? k : 1));
+    return ovf_;
+}
+
 // Kernel selection for one decode call.
-cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
-                          int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status,
-                          cudaStream_t st) {
+cudaError_t launch_decode(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters, int cyc,
+                          uint32_t *state, uint16_t *iters, uint8_t *status) {
+    gb_net *net = cl.net;
     cudaError_t e = cudaErrorNotSupported;
     if (rule == GB_SUM_OF_SUM) {
-        if (sos_tc2_supported(net->s) || sos_tc3_enabled(net->s) || (net->wmap_ok && sos_tc_supported(net->s)))
-            e = launch_decode_sos_tc(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        if (sos_tc2_supported(net->s) || sos_tc3_enabled(net) || (net->wmap_ok && sos_tc_supported(net->s)))
+            e = launch_decode_sos_tc(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
     } else {
-        if (rule == GB_SUM_OF_MAX && som_tc_enabled(net->s))
-            e = launch_som_tc(net, probes, k, max_iters, state, iters, status, st);
-        if (e == cudaErrorNotSupported) e = launch_decode_smem(net, probes, k, rule, max_iters, state, iters, status, st);
-        if (e == cudaErrorNotSupported) e = launch_decode_l2(net, probes, k, rule, max_iters, state, iters, status, st);
+        if (rule == GB_SUM_OF_MAX && som_tc_enabled(net))
+            e = launch_som_tc(cl, probes, k, max_iters, state, iters, status);
+        if (e == cudaErrorNotSupported) e = launch_decode_smem(cl, probes, k, rule, max_iters, state, iters, status);
+        if (e == cudaErrorNotSupported) e = launch_decode_l2(cl, probes, k, rule, max_iters, state, iters, status);
     }
     if (e != cudaErrorNotSupported) return e;
-    return launch_decode_generic(net, probes, k, rule, gamma, max_iters, cyc, state, iters, status, st);
+    return launch_decode_generic(cl, probes, k, rule, gamma, max_iters, cyc, state, iters, status);
 }
 
 }  // namespace gb

@@ -186,9 +186,11 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
 
 }  // namespace
 
-cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k, int rule,
+cudaError_t launch_decode_generic(Call &cl, const uint16_t *probes, int64_t k, int rule,
                                   int gamma, int max_iters, int cyc, uint32_t *state, uint16_t *iters,
-                                  uint8_t *status, cudaStream_t st) {
+                                  uint8_t *status) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     const size_t smem = (size_t)kWarps * 3 * net->s.nw * sizeof(uint32_t);
     int64_t grid = (k + kWarps - 1) / kWarps;
     const int64_t cap = (int64_t)net->sm_count * 8;
@@ -200,7 +202,7 @@ cudaError_t launch_decode_generic(gb_net *net, const uint16_t *probes, int64_t k
     }
     decode_generic_kernel<<<(unsigned)grid, kWarps * 32, smem, st>>>(
         net->s, net->wb, probes, k, rule, gamma, max_iters, cyc, state, iters, status);
-    net->launches += 1;
+    cl.launched();
     return cudaGetLastError();
 }
 

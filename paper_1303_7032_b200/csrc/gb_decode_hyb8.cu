@@ -34,11 +34,16 @@
 namespace gb {
 namespace {
 
+// 768 threads (24 warps, 80 registers).  Measured (round 2, same-box A/B): 1024 threads at 64
+// registers with half-box output staging (W + 32 boxes of 2 KiB fit 227 KiB) is slower -- C3
+// 1.18 vs 1.04 ms, C2 hybrid (10^7) 4.74 vs 3.33 ms: the register cap serialises the staged
+// loads, and each half box waits for the TMA unit to read the previous one.
 constexpr int kNT = 768;            // threads per CTA (one probe each)
 constexpr int kWarps = kNT / 32;
 constexpr int kRowB = 128;          // bytes per W bit row (8 clusters x 16 B)
 constexpr int kClusterB = 128 * kRowB;   // bytes of the 128 rows of one cluster
-constexpr uint32_t kStageB = 32 * 128;   // one warp's output box
+constexpr int kBoxRows = 32;             // probes per TMA output box (one warp)
+constexpr uint32_t kStageB = kBoxRows * 128;   // one warp's output staging box
 constexpr size_t kSmem = 1024 + 1024 * kRowB + (size_t)kWarps * kStageB;
 
 __device__ __forceinline__ void lds4(uint32_t a, uint32_t (&v)[4]) {
@@ -46,6 +51,15 @@ __device__ __forceinline__ void lds4(uint32_t a, uint32_t (&v)[4]) {
 }
 __device__ __forceinline__ void sts4(uint32_t a, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
     asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// Predicated load: v unchanged (zero-initialised by the caller) when p == 0.  No branch, so
+// the loads of one stage issue back to back and their latencies overlap (with `if (x) lds4`
+// the compiler emitted one branch per row and each row's OR waited for its load).
+__device__ __forceinline__ void lds4p(uint32_t p, uint32_t a, uint32_t (&v)[4]) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q ld.shared.v4.u32 {%0,%1,%2,%3}, [%5];\n\t}"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+        : "r"(p), "r"(a));
 }
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
@@ -61,7 +75,7 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
     const uint32_t w_s = sbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t stg = sbase + 1024 * kRowB + warp * kStageB;
-    const uint32_t my_row = stg + lane * 128;
+    const uint32_t my_row = stg + (lane & (kBoxRows - 1)) * 128;
     const uint32_t sw = (uint32_t)(lane & 7);
 
     // W bit rows -> shared memory (row-major, 128 B per row)
@@ -191,38 +205,50 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                 // block c_t of row (c2, 32u + b): rb + (32u + b) * 128
                                 const uint32_t rb = w_s + ((slots >> (4 * sidx)) & 15u) * kClusterB + (ct << 4);
                                 uint32_t h[4] = {0u, 0u, 0u, 0u};
-                                // stage 1: the lowest candidate of each non-empty word
+                                // stage 1: the lowest candidate of each non-empty word (all four
+                                // loads in flight together)
+                                {
+                                    uint32_t r[4][4];
 #pragma unroll
-                                for (int u = 0; u < 4; ++u) {
-                                    const uint32_t x = xr[sidx][u];
-                                    if (x) {
-                                        uint32_t r[4];
-                                        lds4(rb + (u * 32 + lowbit(x)) * kRowB, r);
+                                    for (int u = 0; u < 4; ++u) {
+                                        const uint32_t x = xr[sidx][u];
 #pragma unroll
-                                        for (int v = 0; v < 4; ++v) h[v] |= r[v];
+                                        for (int v = 0; v < 4; ++v) r[u][v] = 0u;
+                                        lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
                                     }
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) h[v] = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
                                 }
                                 uint32_t miss = 0u;
 #pragma unroll
                                 for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
                                 if (miss) {
                                     // stage 2: the highest other candidate of each word holding >= 2
+                                    // (dense W: words 0-1, a cover check, then words 2-3); the loads
+                                    // of a group are predicated and in flight together
 #pragma unroll
-                                    for (int u = 0; u < 4; ++u) {
-                                        if (SPLIT2 && u == 2) {   // dense W: check before words 2, 3
+                                    for (int g = 0; g < (SPLIT2 ? 2 : 1); ++g) {
+                                        if (SPLIT2 && g == 1) {
                                             miss = 0u;
 #pragma unroll
                                             for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
                                             if (!miss) break;
                                         }
-                                        const uint32_t x = xr[sidx][u];
-                                        const uint32_t x2 = x & (x - 1u);
-                                        if (x2) {
-                                            const uint32_t b = highbit(x2);
-                                            uint32_t r[4];
-                                            lds4(rb + (u * 32 + b) * kRowB, r);
+                                        constexpr int kW = SPLIT2 ? 2 : 4;
+                                        uint32_t r[kW][4];
 #pragma unroll
-                                            for (int v = 0; v < 4; ++v) h[v] |= r[v];
+                                        for (int uu = 0; uu < kW; ++uu) {
+                                            const int u = g * kW + uu;
+                                            const uint32_t x = xr[sidx][u];
+                                            const uint32_t x2 = x & (x - 1u);
+#pragma unroll
+                                            for (int v = 0; v < 4; ++v) r[uu][v] = 0u;
+                                            lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[uu]);
+                                        }
+#pragma unroll
+                                        for (int uu = 0; uu < kW; ++uu) {
+#pragma unroll
+                                            for (int v = 0; v < 4; ++v) h[v] |= r[uu][v];
                                         }
                                     }
                                     miss = 0u;
@@ -283,34 +309,38 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
             out_iters[p] = (uint16_t)it;
             out_status[p] = (uint8_t)(bad ? GB_INVALID : status);
         }
-        // the previous box must have been read by the TMA unit before it is overwritten
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        __syncwarp();
-        if (live) {
+        // two half boxes: lanes 0-15, then lanes 16-31 (each waits until the TMA unit has
+        // read the previous box out of the staging buffer)
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                if (bad || !((emask >> c) & 1u)) {
-                    const uint32_t s = bad ? 0xffffffffu : sym[c];
-                    const uint32_t b = 1u << (s & 31u), w = s >> 5;
-                    sts4(my_row + (((uint32_t)c ^ sw) << 4), w == 0 ? b : 0u, w == 1 ? b : 0u, w == 2 ? b : 0u,
-                         w == 3 ? b : 0u);
+        for (int half = 0; half < 32 / kBoxRows; ++half) {
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            if (live && (lane / kBoxRows) == half) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    if (bad || !((emask >> c) & 1u)) {
+                        const uint32_t s = bad ? 0xffffffffu : sym[c];
+                        const uint32_t b = 1u << (s & 31u), w = s >> 5;
+                        sts4(my_row + (((uint32_t)c ^ sw) << 4), w == 0 ? b : 0u, w == 1 ? b : 0u,
+                             w == 2 ? b : 0u, w == 3 ? b : 0u);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (!bad && t < (int)nslot) {
+                        const uint32_t c = (slots >> (4 * t)) & 15u;
+                        sts4(my_row + ((c ^ sw) << 4), xr[t][0], xr[t][1], xr[t][2], xr[t][3]);
+                    }
                 }
             }
-#pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (!bad && t < (int)nslot) {
-                    const uint32_t c = (slots >> (4 * t)) & 15u;
-                    sts4(my_row + ((c ^ sw) << 4), xr[t][0], xr[t][1], xr[t][2], xr[t][3]);
-                }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                    ::"l"((uint64_t)&omap), "r"(0), "r"((int)pb + half * kBoxRows), "r"(stg) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
             }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) {
-            asm volatile(
-                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                ::"l"((uint64_t)&omap), "r"(0), "r"((int)pb), "r"(stg) : "memory");
-            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
         }
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -318,29 +348,31 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
 
 }  // namespace
 
-bool decode_hyb8_supported(const Shape &s, int rule, int64_t k, const void *state) {
+bool decode_hyb8_supported(const gb_net *net, int rule, int64_t k, const void *state) {
+    const Shape &s = net->s;
     return rule == GB_HYBRID && s.C == 8 && s.Wc == 4 && k < (1ll << 31) && ((uintptr_t)state & 15u) == 0 &&
-           !getenv("GB_NO_HYB8");
+           net->opt[kOptHyb8].load(std::memory_order_relaxed) != 0;
 }
 
-// Tensor map of out_state viewed as [k rows][32 words], 32x32 boxes, 128-byte swizzle.
+// Tensor map of out_state viewed as [k rows][32 words], 32 x kBoxRows boxes, 128-byte swizzle.
 static bool encode_out_map(void *state, int64_t k, CUtensorMap *map) {
-    static void *fnp = nullptr;
+    static std::atomic<void *> fnp_cache{nullptr};
+    void *fnp = fnp_cache.load();
     if (!fnp) {
         cudaDriverEntryPointQueryResult q;
         if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
             q != cudaDriverEntryPointSuccess || !fnp) {
             cudaGetLastError();
-            fnp = nullptr;
             return false;
         }
+        fnp_cache.store(fnp);
     }
     using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
     const cuuint64_t dims[2] = {32, (cuuint64_t)k};
     const cuuint64_t strides[1] = {128};
-    const cuuint32_t box[2] = {32, 32};
+    const cuuint32_t box[2] = {32, (cuuint32_t)kBoxRows};
     const cuuint32_t estr[2] = {1, 1};
     return reinterpret_cast<EncodeFn>(fnp)(map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, state, dims, strides, box, estr,
                                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -349,30 +381,26 @@ static bool encode_out_map(void *state, int64_t k, CUtensorMap *map) {
 }
 
 // Narrow (e <= 4) pass of the C = 8 hybrid decode; probes with e > 4 are appended
-// to net->ovf for decode_smem_kernel's list mode (launched by the caller).
-cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                               uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    // the output tensor map depends only on (out_state, k): reuse it across calls
-    CUtensorMap &map = *reinterpret_cast<CUtensorMap *>(net->omap);
-    if (!net->omap_ok || net->omap_ptr != state || net->omap_k != k) {
-        net->omap_ok = encode_out_map(state, k, &map);
-        net->omap_ptr = state;
-        net->omap_k = k;
-        if (!net->omap_ok) return cudaErrorNotSupported;
-    }
+// to `ovf` for decode_smem_kernel's list mode (launched by the caller).
+cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                               uint16_t *iters, uint8_t *status, int64_t *ovf, unsigned long long *ovf_count) {
+    const gb_net *net = cl.net;
+    // the output tensor map is a kernel parameter (copied at launch): encoded per call
+    alignas(64) CUtensorMap map;
+    if (!encode_out_map(state, k, &map)) return cudaErrorNotSupported;
     // Stage 2 in two halves with a cover check between them pays when W is dense (most pairs
     // reach stage 2 and two more rows usually cover): same-box A/B at C3 (density 0.70)
-    // 1.109 -> 1.053 ms, at C2 (density 0.26) 3.33 -> 3.59 ms.  GB_HYB8_SPLIT2=0/1 forces it.
-    const char *fs = getenv("GB_HYB8_SPLIT2");
-    const bool split2 = fs ? (atoi(fs) != 0) : (net->density > 0.5);
+    // 1.109 -> 1.053 ms, at C2 (density 0.26) 3.33 -> 3.59 ms.  GB_OPT_HYB8_SPLIT forces it.
+    const int fs = cl.opt(kOptHyb8Split);
+    const bool split2 = fs >= 0 ? (fs != 0) : (net->density.load(std::memory_order_relaxed) > 0.5);
     auto fn = split2 ? decode_hyb8_kernel<true> : decode_hyb8_kernel<false>;   // compile-time: no cost when off
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
     int64_t grid = (k + kNT - 1) / kNT;
     if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, kNT, kSmem, st>>>(net->wb, probes, k, net->s.L, max_iters, map, iters,
-                                                            status, net->ovf, net->ovf_count);
-    net->launches += 1;
+    fn<<<(unsigned)grid, kNT, kSmem, cl.st>>>(net->wb, probes, k, net->s.L, max_iters, map, iters, status, ovf,
+                                              ovf_count);
+    cl.launched();
     return cudaGetLastError();
 }
 

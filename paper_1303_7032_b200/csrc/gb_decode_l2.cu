@@ -176,9 +176,11 @@ decode_l2_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__res
 }
 
 template <int WC, int RULE>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                     uint16_t *iters, uint8_t *status, cudaStream_t st, const int64_t *list = nullptr,
+cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                     uint16_t *iters, uint8_t *status, const int64_t *list = nullptr,
                      const unsigned long long *list_count = nullptr) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     const size_t smem = (size_t)kL2Warps * 2 * net->s.nw * sizeof(uint32_t);
     auto fn = decode_l2_kernel<WC, RULE>;
     if (smem > 48 * 1024) {
@@ -190,7 +192,7 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
     if (grid > cap || list) grid = cap;
     fn<<<(unsigned)grid, kL2Warps * 32, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status,
                                                     list, list_count);
-    net->launches += 1;
+    cl.launched();
     return cudaGetLastError();
 }
 
@@ -201,49 +203,40 @@ bool decode_l2_supported(const Shape &s, int rule) {
     return s.Wc == 1 || s.Wc == 2 || s.Wc == 4 || s.Wc == 8 || s.Wc == 16;
 }
 
-cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_decode_l2(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                             uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
     if (!decode_l2_supported(net->s, rule)) return cudaErrorNotSupported;
     const bool h = rule == GB_HYBRID;
-    if (decode_l2t_supported(net->s, rule)) {
+    if (decode_l2t_supported(net, rule)) {
         // thread-per-probe kernel; probes with more in-scope clusters than its slots are
         // queued and decoded here by the warp-per-probe kernel in list mode
-        if (net->ovf_cap < k) {
-            cudaFree(net->ovf);
-            net->ovf = nullptr;
-            net->ovf_cap = 0;
-            if (cudaMalloc(&net->ovf, (size_t)k * sizeof(int64_t)) != cudaSuccess) {
-                cudaGetLastError();
-                return cudaErrorMemoryAllocation;
-            }
-            net->ovf_cap = k;
-        }
-        cudaError_t e = cudaMemsetAsync(net->ovf_count, 0, sizeof(unsigned long long), st);
+        int64_t *L = cl.ovf(k);
+        unsigned long long *cnt = cl.counters();
+        if (!L || !cnt) return cl.err;
+        cudaError_t e = launch_decode_l2t(cl, probes, k, rule, max_iters, state, iters, status);
         if (e != cudaSuccess) return e;
-        e = launch_decode_l2t(net, probes, k, rule, max_iters, state, iters, status, st);
-        if (e != cudaSuccess) return e;
-        const int64_t *L = net->ovf;
-        const unsigned long long *LC = net->ovf_count;
+        const unsigned long long *LC = cnt + 1;
         switch (net->s.Wc) {
-            case 4: return h ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
-                             : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
-            case 8: return h ? launch_t<8, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
-                             : launch_t<8, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
-            default: return h ? launch_t<16, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st, L, LC)
-                              : launch_t<16, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st, L, LC);
+            case 4: return h ? launch_t<4, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status, L, LC)
+                             : launch_t<4, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status, L, LC);
+            case 8: return h ? launch_t<8, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status, L, LC)
+                             : launch_t<8, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status, L, LC);
+            default: return h ? launch_t<16, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status, L, LC)
+                              : launch_t<16, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status, L, LC);
         }
     }
     switch (net->s.Wc) {
-        case 1: return h ? launch_t<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 2: return h ? launch_t<2, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<2, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 4: return h ? launch_t<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 8: return h ? launch_t<8, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<8, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        default: return h ? launch_t<16, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                          : launch_t<16, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
+        case 1: return h ? launch_t<1, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<1, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        case 2: return h ? launch_t<2, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<2, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        case 4: return h ? launch_t<4, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<4, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        case 8: return h ? launch_t<8, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<8, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        default: return h ? launch_t<16, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                          : launch_t<16, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
     }
 }
 

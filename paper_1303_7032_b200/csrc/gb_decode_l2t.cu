@@ -244,8 +244,9 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
 }
 
 template <int WC, int RULE, int MAXS>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                     uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                     uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
     // threads per CTA: as many slot-state columns as 192 KiB of shared memory hold (128 KiB at
     // Wc = 16), at most 640 (register budget).  Same-box A/B: 128 KiB / 512 ->
     // 192 KiB / 640 took C4 hybrid 2.59 -> 2.32 ms and C4 SOM 3.33 -> 2.32 ms; Scenario 2
@@ -254,51 +255,46 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
     constexpr int NT0 = (kSmemKB * 1024) / (MAXS * WC * 4);
     constexpr int NT = (NT0 > 640 ? 640 : NT0) / 32 * 32;
     const size_t smem = (size_t)MAXS * WC * NT * sizeof(uint32_t);
-    const size_t need = (size_t)net->sm_count * MAXS * WC * NT * sizeof(uint32_t);
-    if (net->xscratch_bytes < need) {
-        cudaFree(net->xscratch);
-        net->xscratch = nullptr;
-        net->xscratch_bytes = 0;
-        if (cudaMalloc(&net->xscratch, need) != cudaSuccess) {
-            cudaGetLastError();
-            return cudaErrorMemoryAllocation;
-        }
-        net->xscratch_bytes = need;
-    }
+    uint32_t *xscratch = cl.alloc_n<uint32_t>((size_t)net->sm_count * MAXS * WC * NT);
+    int64_t *ovf = cl.ovf(k);
+    unsigned long long *cnt = cl.counters();
+    if (!xscratch || !ovf || !cnt) return cl.err;
     auto fn = decode_l2t_kernel<WC, RULE, MAXS, NT>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int64_t grid = (k + NT - 1) / NT;
     if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, NT, smem, st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status, net->ovf,
-                                         net->ovf_count, net->xscratch);
-    net->launches += 1;
+    fn<<<(unsigned)grid, NT, smem, cl.st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status, ovf,
+                                            cnt + 1, xscratch);
+    cl.launched();
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool decode_l2t_supported(const Shape &s, int rule) {
+bool decode_l2t_supported(const gb_net *net, int rule) {
+    const Shape &s = net->s;
     // measured (round 1, same box, next state in L2 scratch): faster than the warp-per-probe
     // kernel for the hybrid at C4 (2.59 vs 7.92 ms), Scenario 2 (0.270 vs 0.356 ms) and for
     // sum-of-max at C4 (3.33 vs 4.59 ms); sum-of-max at Wc = 16 (16 slots x 64 B per thread)
     // keeps decode_l2_kernel
-    if (getenv("GB_NO_L2T")) return false;
+    if (net->opt[kOptL2t].load(std::memory_order_relaxed) == 0) return false;
     if (rule == GB_SUM_OF_SUM || s.C > kMaxC16) return false;
     if (rule == GB_SUM_OF_MAX) return s.Wc == 4 || s.Wc == 8;
     return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;
 }
 
-cudaError_t launch_decode_l2t(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    if (!decode_l2t_supported(net->s, rule)) return cudaErrorNotSupported;
+cudaError_t launch_decode_l2t(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                              uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    if (!decode_l2t_supported(net, rule)) return cudaErrorNotSupported;
     const bool h = rule == GB_HYBRID;
     switch (net->s.Wc) {
-        case 4: return h ? launch_t<4, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<4, GB_SUM_OF_MAX, 16>(net, probes, k, max_iters, state, iters, status, st);
-        case 8: return h ? launch_t<8, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
-                         : launch_t<8, GB_SUM_OF_MAX, 16>(net, probes, k, max_iters, state, iters, status, st);
-        default: return h ? launch_t<16, GB_HYBRID, 8>(net, probes, k, max_iters, state, iters, status, st)
+        case 4: return h ? launch_t<4, GB_HYBRID, 8>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<4, GB_SUM_OF_MAX, 16>(cl, probes, k, max_iters, state, iters, status);
+        case 8: return h ? launch_t<8, GB_HYBRID, 8>(cl, probes, k, max_iters, state, iters, status)
+                         : launch_t<8, GB_SUM_OF_MAX, 16>(cl, probes, k, max_iters, state, iters, status);
+        default: return h ? launch_t<16, GB_HYBRID, 8>(cl, probes, k, max_iters, state, iters, status)
                           : cudaErrorNotSupported;
     }
 }

@@ -424,9 +424,10 @@ size_t smem_bytes(const Shape &s, int wc, int maxs, int nt) {
 }
 
 template <int WC, int RULE, int MAXS, int NT>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                      uint16_t *iters, uint8_t *status, const int64_t *list, const unsigned long long *list_count,
-                     int64_t *ovf, unsigned long long *ovf_count, cudaStream_t st) {
+                     int64_t *ovf, unsigned long long *ovf_count) {
+    const gb_net *net = cl.net;
     const Shape &s = net->s;
     const size_t smem = smem_bytes(s, WC, MAXS, NT);
     auto fn = decode_smem_kernel<WC, RULE, MAXS, NT>;
@@ -434,44 +435,35 @@ cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int max_ite
     if (e != cudaSuccess) return e;
     int64_t grid = list ? net->sm_count : (k + NT - 1) / NT;
     if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, NT, smem, st>>>(s, net->wb, probes, k, max_iters, state, iters, status, list, list_count,
-                                         ovf, ovf_count);
-    net->launches += 1;
+    fn<<<(unsigned)grid, NT, smem, cl.st>>>(s, net->wb, probes, k, max_iters, state, iters, status, list, list_count,
+                                            ovf, ovf_count);
+    cl.launched();
     return cudaGetLastError();
 }
 
 template <int WC, int RULE>
-cudaError_t launch_rule(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                        uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_rule(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                        uint16_t *iters, uint8_t *status) {
     if (RULE == GB_SUM_OF_MAX)   // every probe needs all C slots
-        return launch_t<WC, RULE, 8, kSomThreads>(net, probes, k, max_iters, state, iters, status, nullptr,
-                                                  nullptr, nullptr, nullptr, st);
-    if (net->s.C <= 4)
-        return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, nullptr,
-                                                   nullptr, nullptr, nullptr, st);
+        return launch_t<WC, RULE, 8, kSomThreads>(cl, probes, k, max_iters, state, iters, status, nullptr,
+                                                  nullptr, nullptr, nullptr);
+    if (cl.net->s.C <= 4)
+        return launch_t<WC, RULE, 8, kWideThreads>(cl, probes, k, max_iters, state, iters, status, nullptr,
+                                                   nullptr, nullptr, nullptr);
     // hybrid: probes with e <= 4 on the narrow (more threads) instance, the rest queued
     // for the wide one (list mode)
-    if (net->ovf_cap < k) {
-        cudaFree(net->ovf);
-        net->ovf = nullptr;
-        net->ovf_cap = 0;
-        if (cudaMalloc(&net->ovf, (size_t)k * sizeof(int64_t)) != cudaSuccess) {
-            cudaGetLastError();
-            return cudaErrorMemoryAllocation;
-        }
-        net->ovf_cap = k;
-    }
-    cudaError_t e = cudaMemsetAsync(net->ovf_count, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    e = cudaErrorNotSupported;
-    if (WC == 4 && RULE == GB_HYBRID && decode_hyb8_supported(net->s, RULE, k, state))
-        e = launch_decode_hyb8(net, probes, k, max_iters, state, iters, status, st);
+    int64_t *ovf = cl.ovf(k);
+    unsigned long long *cnt = cl.counters();
+    if (!ovf || !cnt) return cl.err;
+    cudaError_t e = cudaErrorNotSupported;
+    if (WC == 4 && RULE == GB_HYBRID && decode_hyb8_supported(cl.net, RULE, k, state))
+        e = launch_decode_hyb8(cl, probes, k, max_iters, state, iters, status, ovf, cnt + 1);
     if (e == cudaErrorNotSupported)   // other shapes, or no tensor map for this output buffer
-        e = launch_t<WC, RULE, 4, kNarrowThreads>(net, probes, k, max_iters, state, iters, status, nullptr, nullptr,
-                                                  net->ovf, net->ovf_count, st);
+        e = launch_t<WC, RULE, 4, kNarrowThreads>(cl, probes, k, max_iters, state, iters, status, nullptr, nullptr,
+                                                  ovf, cnt + 1);
     if (e != cudaSuccess) return e;
-    return launch_t<WC, RULE, 8, kWideThreads>(net, probes, k, max_iters, state, iters, status, net->ovf,
-                                               net->ovf_count, nullptr, nullptr, st);
+    return launch_t<WC, RULE, 8, kWideThreads>(cl, probes, k, max_iters, state, iters, status, ovf, cnt + 1,
+                                               nullptr, nullptr);
 }
 
 }  // namespace
@@ -485,18 +477,18 @@ bool decode_smem_supported(const Shape &s, int rule) {
 }
 
 // Returns cudaErrorNotSupported when the shape does not fit this kernel.
-cudaError_t launch_decode_smem(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                               uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    const Shape &s = net->s;
+cudaError_t launch_decode_smem(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                               uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const Shape &s = cl.net->s;
     if (!decode_smem_supported(s, rule)) return cudaErrorNotSupported;
     const bool hyb = (rule == GB_HYBRID);
     switch (s.Wc) {
-        case 1: return hyb ? launch_rule<1, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                           : launch_rule<1, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        case 2: return hyb ? launch_rule<2, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                           : launch_rule<2, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
-        default: return hyb ? launch_rule<4, GB_HYBRID>(net, probes, k, max_iters, state, iters, status, st)
-                            : launch_rule<4, GB_SUM_OF_MAX>(net, probes, k, max_iters, state, iters, status, st);
+        case 1: return hyb ? launch_rule<1, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                           : launch_rule<1, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        case 2: return hyb ? launch_rule<2, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                           : launch_rule<2, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
+        default: return hyb ? launch_rule<4, GB_HYBRID>(cl, probes, k, max_iters, state, iters, status)
+                            : launch_rule<4, GB_SUM_OF_MAX>(cl, probes, k, max_iters, state, iters, status);
     }
 }
 

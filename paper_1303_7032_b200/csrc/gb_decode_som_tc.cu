@@ -282,46 +282,51 @@ bool plan_som(const Shape &s, SomParams &P, size_t &smem) {
 }
 
 template <int WC>
-cudaError_t launch_som_t(gb_net *net, const SomParams &P, size_t smem, const uint16_t *probes, int64_t k,
-                         int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_som_t(Call &cl, const SomParams &P, size_t smem, const uint16_t *probes, int64_t k,
+                         int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     auto fn = som_tc_kernel<WC>;
     if (smem < 120 * 1024) smem = 120 * 1024;   // one CTA per SM: it owns all 512 TMEM columns
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
+    unsigned long long *queue = cl.counters();
+    if (!queue) return cl.err;
     fn<<<grid, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_som), P, probes, k,
-                                max_iters, net->queue, state, iters, status);
-    net->launches += 1;
+                                max_iters, queue, state, iters, status);
+    cl.launched();
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool som_tc_enabled(const Shape &s) {
-    const char *env = getenv("GB_SOM_TC");
-    if (!env || env[0] != '1') return false;
+bool som_tc_enabled(const gb_net *net) {
+    if (net->opt[kOptSomTensor].load(std::memory_order_relaxed) != 1) return false;
     SomParams P;
     size_t smem;
-    return plan_som(s, P, smem);
+    return plan_som(net->s, P, smem);
 }
 
-cudaError_t launch_som_tc(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                          uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_som_tc(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                          uint16_t *iters, uint8_t *status) {
+    gb_net *net = cl.net;
     SomParams P;
     size_t smem;
     if (!plan_som(net->s, P, smem)) return cudaErrorNotSupported;
-    if (!net->wmap_som_ok) {   // W8 (no gamma: the rule only tests counts > 0), box = NP rows
-        net->wmap_som_ok = sos_encode_map(net, net->w8, P.NP, net->wmap_som);
-        if (!net->wmap_som_ok) return cudaErrorNotSupported;
+    {
+        std::lock_guard<std::mutex> lk(net->som_mu);
+        if (!net->wmap_som_ok) {   // W8 (no gamma: the rule only tests counts > 0), box = NP rows
+            net->wmap_som_ok = sos_encode_map(net, net->w8, P.NP, net->wmap_som);
+            if (!net->wmap_som_ok) return cudaErrorNotSupported;
+        }
     }
     switch (net->s.Wc) {
-        case 1: return launch_som_t<1>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        case 2: return launch_som_t<2>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        case 4: return launch_som_t<4>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        default: return launch_som_t<8>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        case 1: return launch_som_t<1>(cl, P, smem, probes, k, max_iters, state, iters, status);
+        case 2: return launch_som_t<2>(cl, P, smem, probes, k, max_iters, state, iters, status);
+        case 4: return launch_som_t<4>(cl, P, smem, probes, k, max_iters, state, iters, status);
+        default: return launch_som_t<8>(cl, P, smem, probes, k, max_iters, state, iters, status);
     }
 }
 

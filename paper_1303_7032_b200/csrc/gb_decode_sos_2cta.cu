@@ -369,14 +369,16 @@ bool plan_pair(const Shape &s, int gamma_epi, Pair2Params &P, size_t &smem) {
 }
 
 template <int WC>
-cudaError_t launch_pair_t(gb_net *net, const Pair2Params &P, size_t smem, const uint16_t *probes, int64_t k,
-                          int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_pair_t(Call &cl, const void *map, const Pair2Params &P, size_t smem, const uint16_t *probes,
+                          int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     auto fn = sos_tc2x2_kernel<WC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // pairs that can be resident at once (TPC pairing can leave SMs unpaired)
-    static int max_clusters[9] = {0};
-    if (max_clusters[WC] == 0) {
+    static std::atomic<int> max_clusters[9];
+    if (max_clusters[WC].load() == 0) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -393,26 +395,25 @@ cudaError_t launch_pair_t(gb_net *net, const Pair2Params &P, size_t smem, const 
             cudaGetLastError();
             n = net->sm_count / 2;
         }
-        max_clusters[WC] = n;
+        max_clusters[WC].store(n);
     }
     const int64_t npairs = (k + 2 * kTM - 1) / (2 * kTM);
-    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC]));
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    fn<<<2 * pairs, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_g2), P, probes, k,
-                                     max_iters, net->queue, state, iters, status);
-    net->launches += 1;
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC].load()));
+    unsigned long long *queue = cl.counters();
+    if (!queue) return cl.err;
+    fn<<<2 * pairs, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(map), P, probes, k,
+                                     max_iters, queue, state, iters, status);
+    cl.launched();
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool sos_2cta_enabled(const Shape &s) {
-    const char *env = getenv("GB_SOS_2CTA");
-    if (env && env[0] == '0') return false;
+bool sos_2cta_enabled(const gb_net *net) {
+    if (net->opt[kOptSosPair].load(std::memory_order_relaxed) == 0) return false;
     Pair2Params P;
     size_t smem;
-    return plan_pair(s, 0, P, smem);
+    return plan_pair(net->s, 0, P, smem);
 }
 
 int sos_2cta_box_rows(const Shape &s) {
@@ -421,8 +422,9 @@ int sos_2cta_box_rows(const Shape &s) {
     return plan_pair(s, 0, P, smem) ? P.BR : 0;
 }
 
-cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, int cyc, const uint16_t *probes, int64_t k, int max_iters,
-                            uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_sos_2cta(Call &cl, const void *map, int gamma_epi, int cyc, const uint16_t *probes, int64_t k,
+                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
     Pair2Params P;
     size_t smem;
     if (!plan_pair(net->s, gamma_epi, P, smem)) return cudaErrorNotSupported;
@@ -430,11 +432,11 @@ cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, int cyc, const uint16_t 
     // one CTA per SM: two 512-column TMEM allocations on one SM could deadlock across pairs
     if (smem < 120 * 1024) smem = 120 * 1024;
     switch (net->s.Wc) {
-        case 1: return launch_pair_t<1>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        case 2: return launch_pair_t<2>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        case 3: return launch_pair_t<3>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        case 4: return launch_pair_t<4>(net, P, smem, probes, k, max_iters, state, iters, status, st);
-        default: return launch_pair_t<8>(net, P, smem, probes, k, max_iters, state, iters, status, st);
+        case 1: return launch_pair_t<1>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
+        case 2: return launch_pair_t<2>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
+        case 3: return launch_pair_t<3>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
+        case 4: return launch_pair_t<4>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
+        default: return launch_pair_t<8>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
     }
 }
 

@@ -633,38 +633,30 @@ bool plan(const Shape &s, SosParams &P, size_t &smem) {
 }
 
 template <int WC>
-cudaError_t launch_t(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters, int cyc,
-                     uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int gamma, int max_iters, int cyc,
+                     uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     SosParams P;
     size_t smem;
     if (!plan(net->s, P, smem)) return cudaErrorNotSupported;
     if (!net->wmap_ok) return cudaErrorNotSupported;
     auto fn = sos_tc_kernel<WC>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     if (smem < 120 * 1024) smem = 120 * 1024;   // one CTA per SM: it owns all 512 TMEM columns
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    uint32_t *vscratch = nullptr;
     if (P.v_global) {
-        const size_t need = (size_t)net->sm_count * 2 * net->s.nw * kTM * sizeof(uint32_t);
-        if (net->vscratch_bytes < need) {
-            cudaFree(net->vscratch);
-            net->vscratch = nullptr;
-            net->vscratch_bytes = 0;
-            if (cudaMalloc(&net->vscratch, need) != cudaSuccess) {
-                cudaGetLastError();
-                return cudaErrorMemoryAllocation;
-            }
-            net->vscratch_bytes = need;
-        }
+        vscratch = cl.alloc_n<uint32_t>((size_t)net->sm_count * 2 * net->s.nw * kTM);
+        if (!vscratch) return cl.err;
     }
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
+    unsigned long long *queue = cl.counters();
+    if (!queue) return cl.err;
     fn<<<grid, kThreads, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap), P, probes, k,
-                                     gamma, max_iters, cyc, net->queue, net->vscratch, state, iters, status);
-    net->launches += 1;
+                                     gamma, max_iters, cyc, queue, vscratch, state, iters, status);
+    cl.launched();
     return cudaGetLastError();
 }
 
@@ -677,59 +669,9 @@ bool sos_tc_supported(const Shape &s) {
     return plan(s, P, smem);
 }
 
-// Encode the TMA descriptor of W8 (n_p x n_p u8, row-major): box 128 B x BR
-// rows, 128-byte swizzle.  Called at gb_create (W8's address never changes).
-bool sos_tc_make_map(gb_net *net) {
-    net->wmap_ok = false;
-    SosParams P;
-    size_t smem;
-    if (!plan(net->s, P, smem)) return false;
-    void *fnp = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fnp) {
-        cudaGetLastError();
-        return false;
-    }
-    using EncodeFn = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-    const cuuint64_t dims[2] = {(cuuint64_t)net->s.np, (cuuint64_t)net->s.np};
-    const cuuint64_t strides[1] = {(cuuint64_t)net->s.np};
-    const cuuint32_t box[2] = {(cuuint32_t)kKB, (cuuint32_t)P.BR};
-    const cuuint32_t estr[2] = {1, 1};
-    alignas(64) CUtensorMap map;
-    CUresult r = reinterpret_cast<EncodeFn>(fnp)(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8,
-                                                 2, net->w8, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    static_assert(sizeof(CUtensorMap) == sizeof(net->wmap), "CUtensorMap size");
-    memcpy(net->wmap, &map, sizeof map);
-    net->wmap_ok = (r == CUDA_SUCCESS);
-    return net->wmap_ok;
-}
-
-namespace {
-
-template <int WC>
-cudaError_t launch2_t(gb_net *net, const Sos2Params &P, size_t smem, const uint16_t *probes, int64_t k,
-                      int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
-    auto fn = sos_tc2_kernel<WC>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    const int64_t ntiles = (k + kTM - 1) / kTM;
-    const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    fn<<<grid, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(net->wmap_g), P, probes, k,
-                                max_iters, net->queue, state, iters, status);
-    net->launches += 1;
-    return cudaGetLastError();
-}
-
-}  // namespace
-
-bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
+// TMA descriptor of an n_p x n_p u8 matrix (row-major) at gaddr: box 128 B x box_rows rows,
+// 128-byte swizzle.
+bool sos_encode_map(const gb_net *net, void *gaddr, int box_rows, unsigned char *out) {
     void *fnp = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fnp, cudaEnableDefault, &q) != cudaSuccess ||
@@ -745,12 +687,45 @@ bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out) 
     const cuuint32_t box[2] = {(cuuint32_t)kKB, (cuuint32_t)box_rows};
     const cuuint32_t estr[2] = {1, 1};
     alignas(64) CUtensorMap map;
+    static_assert(sizeof(CUtensorMap) == 128, "CUtensorMap size");
     CUresult r = reinterpret_cast<EncodeFn>(fnp)(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, gaddr, dims, strides, box,
                                                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     memcpy(out, &map, sizeof map);
     return r == CUDA_SUCCESS;
 }
+
+// TMA descriptor of W8 for the 4-warp kernel (box rows from plan).  Called at gb_create
+// (W8's address never changes).
+bool sos_tc_make_map(gb_net *net) {
+    net->wmap_ok = false;
+    SosParams P;
+    size_t smem;
+    if (!plan(net->s, P, smem)) return false;
+    net->wmap_ok = sos_encode_map(net, net->w8, P.BR, net->wmap);
+    return net->wmap_ok;
+}
+
+namespace {
+
+template <int WC>
+cudaError_t launch2_t(Call &cl, const void *map, const Sos2Params &P, size_t smem, const uint16_t *probes, int64_t k,
+                      int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    auto fn = sos_tc2_kernel<WC>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int64_t ntiles = (k + kTM - 1) / kTM;
+    const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
+    unsigned long long *queue = cl.counters();
+    if (!queue) return cl.err;
+    fn<<<grid, 192, smem, cl.st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(map), P, probes, k,
+                                   max_iters, queue, state, iters, status);
+    cl.launched();
+    return cudaGetLastError();
+}
+
+}  // namespace
 
 bool sos_tc2_supported(const Shape &s) {
     Sos2Params P;
@@ -759,84 +734,110 @@ bool sos_tc2_supported(const Shape &s) {
     return plan2(s, 1, P, smem);
 }
 
-// W8g = W8 + gamma*I (the B operand of the warp-specialised kernels), rebuilt after a
-// seal or a gamma change; gamma > 255 is added in the epilogue instead (B stays W8).
-static cudaError_t ensure_w8g(gb_net *net, int gamma, cudaStream_t st) {
-    if (!net->w8g) {
-        if (cudaMalloc(&net->w8g, (size_t)net->s.np * net->s.np) != cudaSuccess) {
-            cudaGetLastError();
-            net->w8g = nullptr;
-            return cudaErrorMemoryAllocation;
-        }
-        net->w8g_gen = ~0ull;
-    }
+// W8g = W8 + gamma*I, the B operand of the warp-specialised kernels: one variant per
+// (seal generation, folded gamma), built by diag_kernel on the first call that needs it and
+// shared by later calls on any stream (they wait on its `ready` event).  gamma > 255 is added
+// in the epilogue instead (variant gfold = 0, B = W8 with a zero diagonal).  Concurrent
+// decodes with different gammas get different variants; a fifth live gamma evicts the least
+// recently used variant after a device synchronisation (a kernel may still read it).
+cudaError_t gamma_operand(Call &cl, int gamma, int box_rows, const void **map) {
+    gb_net *net = cl.net;
     const int gfold = gamma > 255 ? 0 : gamma;
-    if (net->w8g_gen != net->seal_gen || net->w8g_gamma != gfold) {
-        diag_kernel<<<net->sm_count * 4, 256, 0, st>>>(net->s, net->w8, net->w8g, gfold);
-        net->launches += 1;
+    std::lock_guard<std::mutex> lk(net->gmu);
+    GammaVariant *v = nullptr;
+    for (auto &g : net->gvar)
+        if (g.gfold == gfold && g.gen == net->seal_gen && g.w8g) v = &g;
+    if (!v) {
+        GammaVariant *stale = nullptr, *lru = nullptr;
+        for (auto &g : net->gvar) {
+            if (!g.w8g || g.gen != net->seal_gen) {
+                if (!stale) stale = &g;
+            } else if (!lru || g.last_use < lru->last_use) {
+                lru = &g;
+            }
+        }
+        v = stale ? stale : lru;
+        if (!stale) {   // evicting a live variant: another stream may still read it
+            cudaError_t e = cudaDeviceSynchronize();
+            if (e != cudaSuccess) return e;
+        }
+        if (!v->w8g) {
+            if (cudaMalloc(&v->w8g, (size_t)net->s.np * net->s.np) != cudaSuccess) {
+                cudaGetLastError();
+                v->w8g = nullptr;
+                return cudaErrorMemoryAllocation;
+            }
+            if (cudaEventCreateWithFlags(&v->ready, cudaEventDisableTiming) != cudaSuccess) return cudaErrorUnknown;
+            v->nmaps = 0;   // maps depend only on the (fixed) w8g address and box rows
+        }
+        v->gfold = gfold;
+        v->gen = net->seal_gen;
+        diag_kernel<<<net->sm_count * 4, 256, 0, cl.st>>>(net->s, net->w8, v->w8g, gfold);
+        cl.launched();
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        net->w8g_gen = net->seal_gen;
-        net->w8g_gamma = gfold;
+        e = cudaEventRecord(v->ready, cl.st);
+        if (e != cudaSuccess) return e;
+    } else {
+        cudaError_t e = cudaStreamWaitEvent(cl.st, v->ready, 0);   // built on another call's stream
+        if (e != cudaSuccess) return e;
     }
+    v->last_use = ++net->guse;
+    int mi = -1;
+    for (int i = 0; i < v->nmaps; ++i)
+        if (v->map_rows[i] == box_rows) mi = i;
+    if (mi < 0) {
+        if (v->nmaps == 4) return cudaErrorNotSupported;
+        mi = v->nmaps;
+        if (!sos_encode_map(net, v->w8g, box_rows, v->maps[mi])) return cudaErrorNotSupported;
+        v->map_rows[mi] = box_rows;
+        v->nmaps += 1;
+    }
+    *map = v->maps[mi];
     return cudaSuccess;
 }
 
-cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
-                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_decode_sos_tc(Call &cl, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
     Sos2Params P2;
     size_t smem2;
-    if (sos_fp4_enabled(net->s, gamma)) {   // exact 0/1 contraction on e2m1 (n_p <= 1024, Lp <= 128)
-        cudaError_t e = launch_sos_fp4(net, gamma, cyc, probes, k, max_iters, state, iters, status, st);
-        if (e != cudaErrorNotSupported) return e;
-    }
-    if (sos_tc3_enabled(net->s)) {   // 1024 < n_p <= 4096: streamed A tile
-        cudaError_t e = ensure_w8g(net, gamma, st);
-        if (e != cudaSuccess) return e;
+    if (sos_tc3_enabled(net)) {   // 1024 < n_p <= 4096: streamed A tile
         alignas(8) unsigned char pb[64];
         size_t smem3;
-        if (!plan3(net->s, gamma, pb, smem3)) return cudaErrorNotSupported;
-        const int br = plan3_box_rows(pb);   // differs between the pair and the 1-CTA form
-        if (!net->wmap_g3_ok || net->wmap_g3_br != br) {
-            net->wmap_g3_ok = sos_encode_map(net, net->w8g, br, net->wmap_g3);
-            net->wmap_g3_br = br;
-            if (!net->wmap_g3_ok) return cudaErrorNotSupported;
-        }
-        return launch_sos_tc3(net, gamma, cyc, net->wmap_g3, probes, k, max_iters, state, iters, status, st);
+        if (!plan3(net, gamma, pb, smem3)) return cudaErrorNotSupported;
+        const void *map = nullptr;
+        cudaError_t e = gamma_operand(cl, gamma, plan3_box_rows(pb), &map);
+        if (e != cudaSuccess) return e;
+        return launch_sos_tc3(cl, gamma, cyc, map, probes, k, max_iters, state, iters, status);
     }
     if (plan2(net->s, gamma, P2, smem2) &&
         (net->s.Wc == 1 || net->s.Wc == 2 || net->s.Wc == 3 || net->s.Wc == 4 || net->s.Wc == 8)) {
         P2.cyc = cyc;
-        const bool fresh = !net->w8g;
-        cudaError_t e = ensure_w8g(net, gamma, st);
+        const void *map = nullptr;
+        if (sos_2cta_enabled(net)) {
+            cudaError_t e = gamma_operand(cl, gamma, sos_2cta_box_rows(net->s), &map);
+            if (e != cudaSuccess) return e;
+            return launch_sos_2cta(cl, map, gamma > 255 ? gamma : 0, cyc, probes, k, max_iters, state, iters, status);
+        }
+        cudaError_t e = gamma_operand(cl, gamma, P2.BR, &map);
         if (e != cudaSuccess) return e;
-        if (fresh || !net->wmap_g_ok) {
-            net->wmap_g_ok = sos_encode_map(net, net->w8g, P2.BR, net->wmap_g);
-            if (!net->wmap_g_ok) return cudaErrorNotSupported;
-        }
-        if (sos_2cta_enabled(net->s)) {
-            if (!net->wmap_g2_ok) {
-                net->wmap_g2_ok = sos_encode_map(net, net->w8g, sos_2cta_box_rows(net->s), net->wmap_g2);
-                if (!net->wmap_g2_ok) return cudaErrorNotSupported;
-            }
-            return launch_sos_2cta(net, gamma > 255 ? gamma : 0, cyc, probes, k, max_iters, state, iters, status, st);
-        }
         if (smem2 < 120 * 1024) smem2 = 120 * 1024;   // one CTA per SM (512 TMEM columns)
         switch (net->s.Wc) {
-            case 1: return launch2_t<1>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
-            case 2: return launch2_t<2>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
-            case 3: return launch2_t<3>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
-            case 4: return launch2_t<4>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
-            default: return launch2_t<8>(net, P2, smem2, probes, k, max_iters, state, iters, status, st);
+            case 1: return launch2_t<1>(cl, map, P2, smem2, probes, k, max_iters, state, iters, status);
+            case 2: return launch2_t<2>(cl, map, P2, smem2, probes, k, max_iters, state, iters, status);
+            case 3: return launch2_t<3>(cl, map, P2, smem2, probes, k, max_iters, state, iters, status);
+            case 4: return launch2_t<4>(cl, map, P2, smem2, probes, k, max_iters, state, iters, status);
+            default: return launch2_t<8>(cl, map, P2, smem2, probes, k, max_iters, state, iters, status);
         }
     }
     switch (net->s.Wc) {
-        case 1: return launch_t<1>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
-        case 2: return launch_t<2>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
-        case 3: return launch_t<3>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
-        case 4: return launch_t<4>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
-        case 8: return launch_t<8>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
-        case 16: return launch_t<16>(net, probes, k, gamma, max_iters, cyc, state, iters, status, st);
+        case 1: return launch_t<1>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
+        case 2: return launch_t<2>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
+        case 3: return launch_t<3>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
+        case 4: return launch_t<4>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
+        case 8: return launch_t<8>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
+        case 16: return launch_t<16>(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
         default: return cudaErrorNotSupported;
     }
 }

@@ -267,29 +267,21 @@ sos_tc3_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
 }
 
 template <int WC>
-cudaError_t launch3_t(gb_net *net, const Sos3Params &P, size_t smem, const CUtensorMap *map, const uint16_t *probes,
-                      int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch3_t(Call &cl, const Sos3Params &P, size_t smem, const CUtensorMap *map, const uint16_t *probes,
+                      int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     auto fn = sos_tc3_kernel<WC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int64_t ntiles = (k + kTM - 1) / kTM;
     const int grid = (int)std::min<int64_t>(ntiles, net->sm_count);
-    const size_t need = (size_t)net->sm_count * 2 * net->s.nw * kTM * sizeof(uint32_t);
-    if (net->vscratch_bytes < need) {
-        cudaFree(net->vscratch);
-        net->vscratch = nullptr;
-        net->vscratch_bytes = 0;
-        if (cudaMalloc(&net->vscratch, need) != cudaSuccess) {
-            cudaGetLastError();
-            return cudaErrorMemoryAllocation;
-        }
-        net->vscratch_bytes = need;
-    }
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    fn<<<grid, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, net->queue, net->vscratch, state,
+    uint32_t *vscratch = cl.alloc_n<uint32_t>((size_t)net->sm_count * 2 * net->s.nw * kTM);
+    unsigned long long *queue = cl.counters();
+    if (!vscratch || !queue) return cl.err;
+    fn<<<grid, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, queue, vscratch, state,
                                       iters, status);
-    net->launches += 1;
+    cl.launched();
     return cudaGetLastError();
 }
 
@@ -534,14 +526,16 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
 }
 
 template <int WC>
-cudaError_t launch3x2_t(gb_net *net, const Sos3Params &P, size_t smem, const CUtensorMap *map,
+cudaError_t launch3x2_t(Call &cl, const Sos3Params &P, size_t smem, const CUtensorMap *map,
                         const uint16_t *probes, int64_t k, int max_iters, uint32_t *state, uint16_t *iters,
-                        uint8_t *status, cudaStream_t st) {
+                        uint8_t *status) {
+    const gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     auto fn = sos_tc3x2_kernel<WC>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    static int max_clusters[9] = {0};
-    if (max_clusters[WC] == 0) {
+    static std::atomic<int> max_clusters[9];
+    if (max_clusters[WC].load() == 0) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -558,43 +552,33 @@ cudaError_t launch3x2_t(gb_net *net, const Sos3Params &P, size_t smem, const CUt
             cudaGetLastError();
             n = net->sm_count / 2;
         }
-        max_clusters[WC] = n;
+        max_clusters[WC].store(n);
     }
     const int64_t npairs = (k + 2 * kTM - 1) / (2 * kTM);
-    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC]));
-    const size_t need = (size_t)2 * pairs * 2 * net->s.nw * kTM * sizeof(uint32_t);
-    if (net->vscratch_bytes < need) {
-        cudaFree(net->vscratch);
-        net->vscratch = nullptr;
-        net->vscratch_bytes = 0;
-        if (cudaMalloc(&net->vscratch, need) != cudaSuccess) {
-            cudaGetLastError();
-            return cudaErrorMemoryAllocation;
-        }
-        net->vscratch_bytes = need;
-    }
-    e = cudaMemsetAsync(net->queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return e;
-    fn<<<2 * pairs, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, net->queue, net->vscratch, state,
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC].load()));
+    uint32_t *vscratch = cl.alloc_n<uint32_t>((size_t)2 * pairs * 2 * net->s.nw * kTM);
+    unsigned long long *queue = cl.counters();
+    if (!vscratch || !queue) return cl.err;
+    fn<<<2 * pairs, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, queue, vscratch, state,
                                             iters, status);
-    net->launches += 1;
+    cl.launched();
     return cudaGetLastError();
 }
 
 }  // namespace
 
-static bool pair3_enabled() {
-    const char *env = getenv("GB_SOS_2CTA");
-    return !(env && env[0] == '0');
+static bool pair3_enabled(const gb_net *net) {
+    return net->opt[kOptSosPair].load(std::memory_order_relaxed) != 0;
 }
 
-bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
+bool plan3(const gb_net *net, int gamma, void *params, size_t &smem) {
+    const Shape &s = net->s;
     Sos3Params &P = *reinterpret_cast<Sos3Params *>(params);
     if (s.Lp > 256 || s.np <= 1024 || s.np > 4096) return false;
     if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4 && s.Wc != 8) return false;
     P.NP = s.Lp * (256 / s.Lp);
     if (P.NP > s.np) P.NP = s.np;
-    const bool pair = pair3_enabled();
+    const bool pair = pair3_enabled(net);
     // pair: each CTA stages half of every pass (whole clusters -> halves of Lp/2 rows)
     const int rows = pair ? P.NP / 2 : P.NP;
     int br = 256;
@@ -606,7 +590,6 @@ bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
     P.b_stage = (P.b_stage + 1023u) & ~1023u;   // SW128 atoms stay 1024-byte aligned
     const size_t vbytes = (size_t)s.nw * kTM * 4;
     int s_max = pair ? 6 : 4, sa_max = 3;
-    if (const char *env = getenv("GB_TC3_STAGES")) sscanf(env, "%d,%d", &s_max, &sa_max);   // experiments
     for (P.S = s_max; P.S >= 2; --P.S) {
         for (P.SA = sa_max; P.SA >= 2; --P.SA) {
             P.a_off = 0;
@@ -623,37 +606,37 @@ bool plan3(const Shape &s, int gamma, void *params, size_t &smem) {
 static_assert(sizeof(Sos3Params) <= 64, "plan3 params buffer");
 int plan3_box_rows(const void *params) { return reinterpret_cast<const Sos3Params *>(params)->BR; }
 
-bool sos_tc3_pair(const Shape &s) { return sos_tc3_enabled(s) && pair3_enabled(); }
+bool sos_tc3_pair(const gb_net *net) { return sos_tc3_enabled(net) && pair3_enabled(net); }
 
-bool sos_tc3_enabled(const Shape &s) {
-    const char *env = getenv("GB_SOS_TC3");
-    if (env && env[0] == '0') return false;
+bool sos_tc3_enabled(const gb_net *net) {
+    if (net->opt[kOptSosStreamed].load(std::memory_order_relaxed) == 0) return false;
     Sos3Params P;
     size_t smem;
-    return plan3(s, 1, &P, smem);
+    return plan3(net, 1, &P, smem);
 }
 
-cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
-                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st) {
+cudaError_t launch_sos_tc3(Call &cl, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
+                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
     Sos3Params P;
     size_t smem;
-    if (!plan3(net->s, gamma, &P, smem)) return cudaErrorNotSupported;
+    if (!plan3(net, gamma, &P, smem)) return cudaErrorNotSupported;
     P.cyc = cyc;
     const CUtensorMap *m = reinterpret_cast<const CUtensorMap *>(map);
-    if (pair3_enabled()) {
+    if (pair3_enabled(net)) {
         if (smem < 120 * 1024) smem = 120 * 1024;   // one CTA per SM (512 TMEM columns each)
         switch (net->s.Wc) {
-            case 1: return launch3x2_t<1>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-            case 2: return launch3x2_t<2>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-            case 4: return launch3x2_t<4>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-            default: return launch3x2_t<8>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+            case 1: return launch3x2_t<1>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+            case 2: return launch3x2_t<2>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+            case 4: return launch3x2_t<4>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+            default: return launch3x2_t<8>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
         }
     }
     switch (net->s.Wc) {
-        case 1: return launch3_t<1>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-        case 2: return launch3_t<2>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-        case 4: return launch3_t<4>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
-        default: return launch3_t<8>(net, P, smem, m, probes, k, max_iters, state, iters, status, st);
+        case 1: return launch3_t<1>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+        case 2: return launch3_t<2>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+        case 4: return launch3_t<4>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+        default: return launch3_t<8>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
     }
 }
 

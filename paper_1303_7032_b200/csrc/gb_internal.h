@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
+#include <mutex>
+
 #include "../../include/gb.h"
 
 namespace gb {
@@ -20,6 +23,30 @@ enum : unsigned {
     kFlagIntra = 4u,          // edge inside a cluster / on the diagonal
     kFlagPad = 8u,            // edge touching a padding neuron
     kFlagNotBinary = 16u      // W8 byte not in {0,1}
+};
+
+// Seal status as the last CTA of a seal kernel publishes it (mapped pinned host memory).
+struct Status {
+    unsigned long long gen;        // seal generation this status belongs to
+    unsigned long long invalid;    // invalid stored messages since create/clear
+    unsigned flags;                // structural error flags (kFlagAsym | kFlagIntra | ...)
+    unsigned edges;                // set entries of W (both directions)
+};
+
+// Kernel-selection options of a handle (gb_set_option; GB_OPT_* in gb.h).
+constexpr int kNumOptions = 8;
+
+// One W8 + gamma*I operand (gamma folded into the int8 diagonal, 0..255).
+constexpr int kGammaVariants = 4;
+struct GammaVariant {
+    int gfold = -1;
+    unsigned long long gen = ~0ull;   // seal generation it was built from
+    uint8_t *w8g = nullptr;
+    cudaEvent_t ready = nullptr;      // recorded after its build kernel
+    int nmaps = 0;
+    int map_rows[4] = {0, 0, 0, 0};
+    alignas(64) unsigned char maps[4][128];   // CUtensorMaps of w8g, by box rows
+    unsigned long long last_use = 0;
 };
 
 struct Shape {
@@ -39,104 +66,145 @@ struct gb_net {
     int sm_count;
     uint8_t *w8;          // [np][np] u8, row-major
     uint32_t *wb;         // [np][nw] bit rows
-    unsigned long long *dcount;  // 16-byte device status: [0, 8) invalid stored messages,
-    unsigned *dflag;             // [8, 12) error flags (dflag points into the same allocation),
-                                 // [12, 16) edge count of W (both directions, counted by seal)
-    void *hstat;                 // 16-byte pinned copy of the status (gb_seal)
-    double density;              // edges / (C (C-1) L^2) of the sealed W (kernel heuristics)
-    int64_t stored;
-    bool sealed;
-    // host-staging scratch (gb_decode / gb_store with host pointers)
-    void *stage;
-    size_t stage_bytes;
-    cudaStream_t stage_stream[2];
-    cudaEvent_t stage_event[4];
-    int64_t launches;     // kernels launched by this handle (diagnostics)
-    alignas(64) unsigned char wmap[128];   // CUtensorMap of W8 for the tensor-core SOS kernel
-    bool wmap_ok;
-    uint8_t *w8g;                          // W8 + gamma*I (B operand of sos_tc2_kernel), lazily built
-    alignas(64) unsigned char wmap_g[128];
-    alignas(64) unsigned char wmap_g2[128];  // W8g map with the CTA-pair kernel's box (half the rows)
-    bool wmap_g2_ok;
-    bool wmap_g_ok;                          // wmap_g encoded (sos_tc2 / pair kernels)
-    alignas(64) unsigned char wmap_g3[128];  // W8g map with the streamed-A kernel's box
-    bool wmap_g3_ok;
-    int wmap_g3_br;                          // box rows wmap_g3 was encoded with
-    uint8_t *w4;                             // W8 + gamma*I as packed e2m1 (B operand of sos_fp4_kernel)
-    alignas(64) unsigned char w4map[128];
-    unsigned long long w4_gen;
-    int w4_gamma;
-    alignas(64) unsigned char omap[128];     // out_state map of decode_hyb8_kernel (cached per buffer, k)
-    bool omap_ok;
-    const void *omap_ptr;
-    int64_t omap_k;
+    // Device status words (one 32-byte allocation):
+    //   [0, 8) invalid stored messages since create/clear (store kernels; reset by gb_clear)
+    //   [8, 12) structural error flags of the running seal, [12, 16) its edge count,
+    //   [16, 20) CTAs of the running seal that have finished (the last one publishes + resets)
+    unsigned long long *dcount;
+    unsigned *dflag;             // = dcount + 8 bytes
+    gb::Status *hstat;           // mapped pinned host memory: the seal kernel publishes here
+    gb::Status *hstat_dev;       // its device alias
+    cudaEvent_t seal_event;      // recorded after each seal kernel
+    std::mutex smu;              // seal-status resolution (host side)
+    unsigned long long seal_gen = 0;         // seals enqueued (generation of the sealed W)
+    unsigned long long seal_resolved = 0;    // last seal whose status the host has read
+    unsigned long long invalid_reported = 0; // invalid-message count already reported
+    unsigned long long clear_epoch = 0;      // gb_clear calls (they reset the device count)
+    unsigned long long seal_epoch = 0;       // clear_epoch when the latest seal was issued
+    unsigned long long reported_epoch = 0;   // epoch invalid_reported belongs to
+    int seal_rc = 0;                         // outcome of the latest resolved seal
+    char seal_msg[200] = "";
+    std::atomic<double> density{0.0};        // edges / (C (C-1) L^2) of the last resolved seal (heuristics)
+    int64_t stored = 0;
+    std::atomic<bool> sealed{false};         // a seal is enqueued and no W change followed
+    std::atomic<bool> seal_broken{false};    // the last resolved seal found broken invariants
+    // kernel-selection options (gb_set_option), read by decodes
+    std::atomic<int> opt[gb::kNumOptions];
+    // stream-ordered per-call scratch (work counters, overflow lists, state scratch, staging)
+    cudaMemPool_t pool = nullptr;
+    // host-buffer staging (gb_decode / gb_store with host pointers): serialised per handle
+    std::mutex stage_mu;
+    cudaStream_t stage_stream[2] = {nullptr, nullptr};
+    cudaEvent_t stage_event = nullptr;
+    std::atomic<long long> launches{0};      // kernels launched by this handle (diagnostics)
+    alignas(64) unsigned char wmap[128];     // CUtensorMap of W8 for the 4-warp SOS kernel
+    bool wmap_ok = false;
     alignas(64) unsigned char wmap_som[128]; // W8 map for the tensor-core sum-of-max kernel
-    bool wmap_som_ok;
-    int w8g_gamma;
-    unsigned long long seal_gen, w8g_gen;  // W8g is valid for (seal generation, gamma)
-    unsigned long long *queue;             // device work counter (slot-refill kernels)
-    uint32_t *vscratch;                    // SOS state scratch when it does not fit shared memory
-    int64_t *ovf;                          // hybrid probes queued for the wide-slot smem kernel
-    int64_t ovf_cap;
-    unsigned long long *ovf_count;
-    size_t vscratch_bytes;
-    uint32_t *xscratch;                    // next-state scratch of the thread-per-probe L2 kernel
-    size_t xscratch_bytes;
-    uint32_t *spart;                       // per-chunk partial bit matrices of the privatised store
-    size_t spart_bytes;
+    bool wmap_som_ok = false;
+    std::mutex som_mu;
+    // W8 + gamma*I variants (B operand of the warp-specialised SOS kernels), one per folded gamma
+    std::mutex gmu;
+    gb::GammaVariant gvar[gb::kGammaVariants];
+    unsigned long long guse = 0;
 };
 
 namespace gb {
 
-// Launchers (return cudaError_t of the launch).
-cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st);
-cudaError_t launch_seal(const gb_net *net, cudaStream_t st);
-cudaError_t launch_or_bits(gb_net *net, const uint32_t *bits, int64_t count, cudaStream_t st);
+// One store / decode call: the caller's stream and the call's private device scratch,
+// allocated stream-ordered from the handle's memory pool and released (stream-ordered)
+// when the call object goes out of scope.  Nothing a kernel writes lives in the handle,
+// so concurrent decodes on one handle (distinct streams, host threads) cannot race
+// (SURVEY.md §8.b "Concurrency").
+struct Call {
+    gb_net *net;
+    cudaStream_t st;
+    cudaError_t err = cudaSuccess;
+    Call(gb_net *n, cudaStream_t s) : net(n), st(s) {}
+    Call(const Call &) = delete;
+    Call &operator=(const Call &) = delete;
+    ~Call();
+    void *alloc(size_t bytes);     // nullptr on failure (err set)
+    template <class T> T *alloc_n(size_t n) { return static_cast<T *>(alloc(n * sizeof(T))); }
+    // [0] work queue of the slot-refill kernels, [1] overflow count; zeroed once per call
+    unsigned long long *counters();
+    // overflow list of probe indices (k entries) for the two-pass bit kernels
+    int64_t *ovf(int64_t k);
+    int opt(int o) const { return net->opt[o].load(std::memory_order_relaxed); }
+    void launched(int n = 1) { net->launches.fetch_add(n, std::memory_order_relaxed); }
+
+  private:
+    void *blk_[8];
+    int nblk_ = 0;
+    unsigned long long *counters_ = nullptr;
+    int64_t *ovf_ = nullptr;
+};
+
+// Option indices (gb.h GB_OPT_*) and defaults.
+enum : int {
+    kOptSosPair = 0,       // CTA-pair (cta_group::2) sum-of-sum kernels
+    kOptSosStreamed = 1,   // streamed-A sum-of-sum kernel for 1024 < n_p <= 4096
+    kOptSomTensor = 2,     // exact sum-of-max on the tensor cores (N2)
+    kOptHyb8 = 3,          // C = 8 hybrid kernel
+    kOptL2t = 4,           // thread-per-probe L2 bit kernel
+    kOptHyb8Split = 5,     // dense-W stage split of the C = 8 hybrid kernel: -1 auto, 0, 1
+    kOptStoreScatter = 6,  // store with scattered byte writes only (no privatised tiles)
+};
+int option_default(int o);
+
+// Launchers (return cudaError_t of the launch; cudaErrorNotSupported = shape not taken).
+cudaError_t launch_store(Call &cl, const uint16_t *msgs, int64_t m);
+cudaError_t launch_seal(gb_net *net, cudaStream_t st);
+cudaError_t launch_or_bits(Call &cl, const uint32_t *bits, int64_t count);
+int64_t upper_words(const Shape &s);   // words of one packed upper-triangle set
+cudaError_t launch_pack_upper(Call &cl, uint32_t *out);
+cudaError_t launch_or_upper(Call &cl, const uint32_t *sets, int64_t count);
 bool decode_smem_supported(const Shape &s, int rule);
 bool decode_l2_supported(const Shape &s, int rule);
 // thread-per-probe L2 kernel (gb_decode_l2t.cu): probes needing more slots than it
-// holds are appended to net->ovf (decode_l2_kernel decodes them in list mode).
-bool decode_l2t_supported(const Shape &s, int rule);
-cudaError_t launch_decode_l2t(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                              uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
-cudaError_t launch_decode_l2(gb_net *net, const uint16_t *probes, int64_t k, int rule, int max_iters,
-                             uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+// holds are appended to the call's overflow list (decode_l2_kernel decodes them in list mode).
+bool decode_l2t_supported(const gb_net *net, int rule);
+cudaError_t launch_decode_l2t(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                              uint32_t *state, uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode_l2(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                             uint32_t *state, uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode_smem(Call &cl, const uint16_t *probes, int64_t k, int rule, int max_iters,
+                               uint32_t *state, uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode_generic(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma,
+                                  int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
 bool sos_tc_supported(const Shape &s);
 bool sos_tc2_supported(const Shape &s);
 bool sos_tc_make_map(gb_net *net);
-bool sos_encode_map(gb_net *net, void *gaddr, int box_rows, unsigned char *out);
-// CTA-pair (cta_group::2) sum-of-sum kernel, gb_decode_sos_2cta.cu; the caller
-// has built W8g = W8 + gamma*I (gamma_epi = gamma when gamma > 255, else 0).
-bool sos_2cta_enabled(const Shape &s);
+bool sos_encode_map(const gb_net *net, void *gaddr, int box_rows, unsigned char *out);
+// The W8 + gamma*I operand for gamma (folded when <= 255), built (once per seal and
+// gamma) on / ordered before the call's stream, and its tensor map with `box_rows` rows.
+cudaError_t gamma_operand(Call &cl, int gamma, int box_rows, const void **map);
+// CTA-pair (cta_group::2) sum-of-sum kernel, gb_decode_sos_2cta.cu; `map` is the W8 + gamma*I
+// operand (gamma_epi = gamma when gamma > 255, else 0).
+bool sos_2cta_enabled(const gb_net *net);
 int sos_2cta_box_rows(const Shape &s);
-cudaError_t launch_sos_2cta(gb_net *net, int gamma_epi, int cyc, const uint16_t *probes, int64_t k, int max_iters,
-                            uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+cudaError_t launch_sos_2cta(Call &cl, const void *map, int gamma_epi, int cyc, const uint16_t *probes, int64_t k,
+                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status);
 // C = 8, Wc = 4 hybrid decode of the probes with e <= 4 (gb_decode_hyb8.cu); the
-// others are appended to net->ovf.
-bool decode_hyb8_supported(const Shape &s, int rule, int64_t k, const void *state);
-cudaError_t launch_decode_hyb8(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                               uint16_t *iters, uint8_t *status, cudaStream_t st);
-// Streamed-A sum-of-sum kernel for 1024 < n_p <= 4096 (gb_decode_sos_tc3.cu); the
-// caller has built W8g = W8 + gamma*I and its tensor map (box rows from plan3).
-bool plan3(const Shape &s, int gamma, void *params, size_t &smem);
+// others are appended to the overflow list `ovf`.
+bool decode_hyb8_supported(const gb_net *net, int rule, int64_t k, const void *state);
+cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                               uint16_t *iters, uint8_t *status, int64_t *ovf, unsigned long long *ovf_count);
+// Streamed-A sum-of-sum kernel for 1024 < n_p <= 4096 (gb_decode_sos_tc3.cu); `map` is the
+// W8 + gamma*I operand with plan3's box rows.
+bool plan3(const gb_net *net, int gamma, void *params, size_t &smem);
 int plan3_box_rows(const void *params);
-bool sos_tc3_enabled(const Shape &s);
-bool sos_tc3_pair(const Shape &s);   // the streamed-A kernel runs on CTA pairs
-cudaError_t launch_sos_tc3(gb_net *net, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
-                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
+bool sos_tc3_enabled(const gb_net *net);
+bool sos_tc3_pair(const gb_net *net);   // the streamed-A kernel runs on CTA pairs
+cudaError_t launch_sos_tc3(Call &cl, int gamma, int cyc, const void *map, const uint16_t *probes, int64_t k,
+                           int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status);
 // cyc = 1: period-2 cycle exit (GB_FLAG_CYCLE_EXIT) in every sum-of-sum kernel
-// sum-of-sum on block-scaled FP4 tensor cores (gb_decode_sos_fp4.cu)
-bool sos_fp4_enabled(const Shape &s, int gamma);
-cudaError_t launch_sos_fp4(gb_net *net, int gamma, int cyc, const uint16_t *probes, int64_t k, int max_iters,
-                           uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
-// exact sum-of-max on the tensor cores (gb_decode_som_tc.cu, N2), opt-in with GB_SOM_TC=1
-bool som_tc_enabled(const Shape &s);
-cudaError_t launch_som_tc(gb_net *net, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
-                          uint16_t *iters, uint8_t *status, cudaStream_t st);
-cudaError_t launch_decode_sos_tc(gb_net *net, const uint16_t *probes, int64_t k, int gamma, int max_iters,
-                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status, cudaStream_t st);
-cudaError_t launch_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
-                          int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status,
-                          cudaStream_t st);
+// exact sum-of-max on the tensor cores (gb_decode_som_tc.cu, N2), option GB_OPT_SOM_TENSOR
+bool som_tc_enabled(const gb_net *net);
+cudaError_t launch_som_tc(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
+                          uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode_sos_tc(Call &cl, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                                 int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma,
+                          int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
 
 }  // namespace gb

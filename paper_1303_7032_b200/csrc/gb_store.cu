@@ -76,35 +76,59 @@ __device__ __forceinline__ uint32_t pack32(const uint8_t *p, unsigned &nonbin) {
 }
 
 __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *__restrict__ wb,
-                            unsigned *__restrict__ dflag, unsigned *__restrict__ dedges) {
+                            unsigned long long *__restrict__ dcount, Status *__restrict__ hstat,
+                            unsigned long long gen) {
+    unsigned *dflag = reinterpret_cast<unsigned *>(dcount + 1);   // [0] flags, [1] edges, [2] CTAs done
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int nt = s.np / 32;
-    if (warp >= (int64_t)nt * nt) return;
-    const int ti = (int)(warp / nt), tj = (int)(warp - (int64_t)ti * nt);
-    const int i0 = 32 * ti, j0 = 32 * tj;
-    unsigned nonbin = 0u;
-    const uint32_t P = pack32(w8 + (int64_t)(i0 + lane) * s.np + j0, nonbin);   // W8[i0+lane][j0+b]
-    const uint32_t T = pack32(w8 + (int64_t)(j0 + lane) * s.np + i0, nonbin);   // W8[j0+lane][i0+b]
-    uint32_t R = 0u;                                                             // W8[j0+b][i0+lane]
+    if (warp < (int64_t)nt * nt) {
+        const int ti = (int)(warp / nt), tj = (int)(warp - (int64_t)ti * nt);
+        const int i0 = 32 * ti, j0 = 32 * tj;
+        unsigned nonbin = 0u;
+        const uint32_t P = pack32(w8 + (int64_t)(i0 + lane) * s.np + j0, nonbin);   // W8[i0+lane][j0+b]
+        const uint32_t T = pack32(w8 + (int64_t)(j0 + lane) * s.np + i0, nonbin);   // W8[j0+lane][i0+b]
+        uint32_t R = 0u;                                                             // W8[j0+b][i0+lane]
 #pragma unroll 8
-    for (int k = 0; k < 32; ++k) {
-        const uint32_t x = __ballot_sync(0xffffffffu, (T >> k) & 1u);
-        if (lane == k) R = x;
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t x = __ballot_sync(0xffffffffu, (T >> k) & 1u);
+            if (lane == k) R = x;
+        }
+        const int ci = i0 / s.Lp, cj = j0 / s.Lp;
+        const int cb = j0 - cj * s.Lp;   // first column slot of the tile inside cluster cj
+        const uint32_t realc = cb >= s.L ? 0u : (s.L - cb >= 32 ? 0xffffffffu : ((1u << (s.L - cb)) - 1u));
+        const bool realr = (i0 + lane - ci * s.Lp) < s.L;
+        unsigned bad = nonbin ? kFlagNotBinary : 0u;
+        if (P != R) bad |= kFlagAsym;
+        if (P && ci == cj) bad |= kFlagIntra;
+        if ((P & ~realc) || (P && !realr)) bad |= kFlagPad;
+        wb[(int64_t)(i0 + lane) * s.nw + tj] = P;
+        const unsigned anybad = __reduce_or_sync(0xffffffffu, bad);
+        if (lane == 0 && anybad) atomicOr(dflag, anybad);
+        const unsigned ne = __reduce_add_sync(0xffffffffu, (unsigned)__popc(P));   // edges (both directions)
+        if (lane == 0 && ne) atomicAdd(dflag + 1, ne);
     }
-    const int ci = i0 / s.Lp, cj = j0 / s.Lp;
-    const int cb = j0 - cj * s.Lp;   // first column slot of the tile inside cluster cj
-    const uint32_t realc = cb >= s.L ? 0u : (s.L - cb >= 32 ? 0xffffffffu : ((1u << (s.L - cb)) - 1u));
-    const bool realr = (i0 + lane - ci * s.Lp) < s.L;
-    unsigned bad = nonbin ? kFlagNotBinary : 0u;
-    if (P != R) bad |= kFlagAsym;
-    if (P && ci == cj) bad |= kFlagIntra;
-    if ((P & ~realc) || (P && !realr)) bad |= kFlagPad;
-    wb[(int64_t)(i0 + lane) * s.nw + tj] = P;
-    const unsigned anybad = __reduce_or_sync(0xffffffffu, bad);
-    if (lane == 0 && anybad) atomicOr(dflag, anybad);
-    const unsigned ne = __reduce_add_sync(0xffffffffu, (unsigned)__popc(P));   // edges (both directions)
-    if (lane == 0 && ne) atomicAdd(dedges, ne);
+    // the last CTA to finish publishes the status to mapped host memory (no host sync in
+    // gb_seal) and resets the per-seal words for the next seal
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(dflag + 2, 1u) == gridDim.x - 1) {
+            __threadfence();
+            const unsigned long long inv = atomicAdd(dcount, 0ull);
+            const unsigned flags = atomicOr(dflag, 0u), edges = atomicAdd(dflag + 1, 0u);
+            volatile Status *h = hstat;
+            h->invalid = inv;
+            h->flags = flags;
+            h->edges = edges;
+            __threadfence_system();
+            h->gen = gen;
+            __threadfence_system();
+            dflag[0] = 0u;
+            dflag[1] = 0u;
+            dflag[2] = 0u;
+        }
+    }
 }
 
 // ---- privatised store (large m): one CTA = (row cluster c, column-cluster
@@ -227,6 +251,78 @@ __global__ void apply_kernel(Shape s, const uint32_t *__restrict__ part, int chu
     }
 }
 
+// ---- upper-triangle exchange: W is symmetric, so the
+// cluster-pair blocks (a, b) with a < b carry all of it.  Packed layout: blocks in (a, b)
+// lexicographic order, each Lp rows x Wc words of Wb, row-major.
+__device__ __forceinline__ void upper_block(const Shape &s, int64_t q, int &a, int &b) {
+    a = 0;
+    while (q >= s.C - 1 - a) {
+        q -= s.C - 1 - a;
+        ++a;
+    }
+    b = a + 1 + (int)q;
+}
+
+__global__ void pack_upper_kernel(Shape s, const uint32_t *__restrict__ wb, uint32_t *__restrict__ out) {
+    const int64_t per = (int64_t)s.Lp * s.Wc;
+    const int64_t total = per * s.C * (s.C - 1) / 2;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t q = idx / per, rem = idx - q * per;
+        const int r = (int)(rem / s.Wc), w = (int)(rem - (int64_t)r * s.Wc);
+        int a, b;
+        upper_block(s, q, a, b);
+        out[idx] = __ldg(wb + ((int64_t)a * s.Lp + r) * s.nw + b * s.Wc + w);
+    }
+}
+
+// OR 32 bits into the 32 W8 bytes at p (bit k -> byte k); read-modify-write only if any bit.
+__device__ __forceinline__ void or_bytes32(uint8_t *p, uint32_t bits) {
+    if (!bits) return;
+    uint4 *q = reinterpret_cast<uint4 *>(p);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint4 v = q[h];
+        uint32_t x[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t nib = (bits >> (16 * h + 4 * k)) & 15u;
+            x[k] |= (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+        }
+        q[h] = make_uint4(x[0], x[1], x[2], x[3]);
+    }
+}
+
+// One warp per 32x32 tile of an upper block: lane l ORs row i0+l's word over the `count`
+// packed sets, sets W8[i0+l][j0..j0+31], and (after a 32-ballot transpose) the mirror
+// W8[j0+l][i0..i0+31].  Every W8 segment is written by exactly one lane.
+__global__ void or_upper_kernel(Shape s, const uint32_t *__restrict__ sets, int count, uint8_t *__restrict__ w8) {
+    const int64_t per = (int64_t)s.Lp * s.Wc;
+    const int64_t set_words = per * s.C * (s.C - 1) / 2;
+    const int64_t tiles = set_words / 32;   // (Lp / 32) row groups x Wc words per block
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < tiles;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t per_t = per / 32;
+        const int64_t q = t / per_t, rem = t - q * per_t;
+        const int rg = (int)(rem / s.Wc), w = (int)(rem - (int64_t)rg * s.Wc);
+        int a, b;
+        upper_block(s, q, a, b);
+        const int64_t idx = q * per + (int64_t)(rg * 32 + lane) * s.Wc + w;
+        uint32_t bits = 0u;
+        for (int k = 0; k < count; ++k) bits |= __ldg(sets + (int64_t)k * set_words + idx);
+        const int64_t i0 = (int64_t)a * s.Lp + rg * 32, j0 = (int64_t)b * s.Lp + w * 32;
+        or_bytes32(w8 + (i0 + lane) * s.np + j0, bits);
+        uint32_t tr = 0u;
+#pragma unroll 8
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t x = __ballot_sync(0xffffffffu, (bits >> k) & 1u);
+            if (lane == k) tr = x;
+        }
+        or_bytes32(w8 + (j0 + lane) * s.np + i0, tr);
+    }
+}
+
 constexpr size_t kPrivTileMax = GB_PRIV_TILE_KB * 1024;
 
 PrivPlan priv_plan(const Shape &s, int64_t m, int sm_count) {
@@ -246,29 +342,24 @@ PrivPlan priv_plan(const Shape &s, int64_t m, int sm_count) {
 
 }  // namespace
 
-cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStream_t st) {
+cudaError_t launch_store(Call &cl, const uint16_t *msgs, int64_t m) {
+    gb_net *net = cl.net;
+    const cudaStream_t st = cl.st;
     const Shape &s = net->s;
-    // small batches: scattered relaxed byte stores (no tile setup / apply pass)
-    if (m * s.C * (s.C - 1) < (int64_t)s.np * s.nw * 8 || getenv("GB_STORE_SCATTER")) {
+    const PrivPlan p = priv_plan(s, m, net->sm_count);
+    // small batches: scattered relaxed byte stores (no tile setup / apply pass); also when one
+    // cluster-pair block does not fit the privatised tile (Lp > 1024: Lp^2/8 > 128 KiB)
+    if (m * s.C * (s.C - 1) < (int64_t)s.np * s.nw * 8 || cl.opt(kOptStoreScatter) == 1 ||
+        p.tile_bytes > kPrivTileMax + (size_t)s.Lp * 4) {
         const int64_t threads = m * s.C;
         const int block = 256;
         const int64_t grid = (threads + block - 1) / block;
         store_kernel<<<(unsigned)grid, block, 0, st>>>(s, msgs, m, net->w8, net->dcount, net->dflag);
-        net->launches += 1;
+        cl.launched();
         return cudaGetLastError();
     }
-    const PrivPlan p = priv_plan(s, m, net->sm_count);
-    const size_t need = (size_t)p.chunks * s.np * s.nw * sizeof(uint32_t);
-    if (net->spart_bytes < need) {
-        cudaFree(net->spart);
-        net->spart = nullptr;
-        net->spart_bytes = 0;
-        if (cudaMalloc(&net->spart, need) != cudaSuccess) {
-            cudaGetLastError();
-            return cudaErrorMemoryAllocation;
-        }
-        net->spart_bytes = need;
-    }
+    uint32_t *spart = cl.alloc_n<uint32_t>((size_t)p.chunks * s.np * s.nw);
+    if (!spart) return cl.err;
     // vector loads of whole messages when C = 8, 16, 24, 32 and rows are 16-byte aligned
     const int nv = ((s.C % 8) == 0 && s.C <= 32 && ((uintptr_t)msgs & 15u) == 0) ? s.C / 8 : 0;
     auto fn = nv == 1 ? store_priv_kernel<1> : nv == 2 ? store_priv_kernel<2>
@@ -276,26 +367,46 @@ cudaError_t launch_store(gb_net *net, const uint16_t *msgs, int64_t m, cudaStrea
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tile_bytes);
     if (e != cudaSuccess) return e;
     fn<<<(unsigned)(p.chunks * p.tiles), GB_PRIV_NT, p.tile_bytes, st>>>(
-        s, msgs, m, p.G, p.ngroups, p.tiles, p.per_chunk, net->spart, net->dcount, net->dflag);
+        s, msgs, m, p.G, p.ngroups, p.tiles, p.per_chunk, spart, net->dcount, net->dflag);
     const int64_t total = (int64_t)s.np * s.nw;
-    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, net->spart, p.chunks, net->w8);
-    net->launches += 2;
+    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(s, spart, p.chunks, net->w8);
+    cl.launched(2);
     return cudaGetLastError();
 }
 
 // OR `count` packed bit matrices into W8 (the apply pass of the privatised store).
-cudaError_t launch_or_bits(gb_net *net, const uint32_t *bits, int64_t count, cudaStream_t st) {
-    const int64_t total = (int64_t)net->s.np * net->s.nw;
-    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(net->s, bits, (int)count, net->w8);
-    net->launches += 1;
+cudaError_t launch_or_bits(Call &cl, const uint32_t *bits, int64_t count) {
+    const int64_t total = (int64_t)cl.net->s.np * cl.net->s.nw;
+    apply_kernel<<<(unsigned)((total + 255) / 256), 256, 0, cl.st>>>(cl.net->s, bits, (int)count, cl.net->w8);
+    cl.launched();
     return cudaGetLastError();
 }
 
-cudaError_t launch_seal(const gb_net *net, cudaStream_t st) {
+int64_t upper_words(const Shape &s) { return (int64_t)s.Lp * s.Wc * s.C * (s.C - 1) / 2; }
+
+cudaError_t launch_pack_upper(Call &cl, uint32_t *out) {
+    const int64_t total = upper_words(cl.net->s);
+    const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)cl.net->sm_count * 8);
+    pack_upper_kernel<<<(unsigned)grid, 256, 0, cl.st>>>(cl.net->s, cl.net->wb, out);
+    cl.launched();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_or_upper(Call &cl, const uint32_t *sets, int64_t count) {
+    const int64_t warps = upper_words(cl.net->s) / 32;
+    const int64_t grid = std::min<int64_t>((warps * 32 + 255) / 256, (int64_t)cl.net->sm_count * 16);
+    or_upper_kernel<<<(unsigned)grid, 256, 0, cl.st>>>(cl.net->s, sets, (int)count, cl.net->w8);
+    cl.launched();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seal(gb_net *net, cudaStream_t st) {
     const int64_t warps = (int64_t)(net->s.np / 32) * (net->s.np / 32);
     const int block = 256;
     const int64_t grid = (warps * 32 + block - 1) / block;
-    seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dflag, net->dflag + 1);
+    seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dcount, net->hstat_dev,
+                                                  net->seal_gen);
+    net->launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
 

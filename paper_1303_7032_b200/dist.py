@@ -15,7 +15,14 @@ box, gloo in the CPU tests).  Nothing here computes any part of the method:
   partial W (bit rows Wb, n_p^2/8 bytes), the Wb's are all-gathered, and every
   rank ORs all of them into its W8 (gb_or_bits) -- per rank (G-1) n_p^2/8 bytes
   received instead of the ring all-reduce's 2 (G-1)/G n_p^2 bytes of u8;
-* alternatively W is built once and replicated with a broadcast.
+* for decode (north_star, BASELINE config C3) W is built on one rank and
+  replicated: the root stores the messages and seals, its packed rows Wb
+  (n_p^2/8 bytes: 128 KiB at c=8 l=128) are broadcast, and every other rank
+  ORs them into its cleared W8 (gb_or_bits) and seals -- all ranks end with
+  byte-identical W8 / Wb.
+
+Collectives on a gloo group (the CPU tests and the one-GPU multi-rank test)
+take a host round trip, so the same code runs with NCCL on the GPU box.
 """
 from __future__ import annotations
 
@@ -50,15 +57,60 @@ def merge_weights_(w8: torch.Tensor, group=None) -> torch.Tensor:
     """In-place all-reduce MAX of the u8 weight matrix (= OR of the partial W's)."""
     if w8.dtype != torch.uint8:
         raise TypeError("merge_weights_ needs the uint8 W8 matrix (MAX on packed bits is not OR)")
-    if dist.is_initialized():
-        dist.all_reduce(w8, op=dist.ReduceOp.MAX, group=group)
+    if dist.is_available() and dist.is_initialized():
+        if w8.is_cuda and not _is_nccl(group):
+            h = w8.detach().cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.MAX, group=group)
+            w8.copy_(h)
+        else:
+            dist.all_reduce(w8, op=dist.ReduceOp.MAX, group=group)
     return w8
+
+
+def _is_nccl(group=None):
+    return dist.get_backend(group) == "nccl"
+
+
+def broadcast_(t: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
+    """In-place broadcast of ``t`` from rank ``src`` (NCCL on the tensor's device; gloo via host)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return t
+    if t.is_cuda and not _is_nccl(group):
+        h = t.detach().cpu()
+        dist.broadcast(h, src=src, group=group)
+        t.copy_(h)
+    else:
+        dist.broadcast(t, src=src, group=group)
+    return t
 
 
 def broadcast_weights_(w8: torch.Tensor, src: int = 0, group=None) -> torch.Tensor:
-    if dist.is_initialized():
-        dist.broadcast(w8, src=src, group=group)
-    return w8
+    """Replicate the u8 W8 of rank ``src`` (after this, call seal on every rank)."""
+    return broadcast_(w8, src, group)
+
+
+def replicated_store(net, msgs, src: int = 0, group=None, stream=None):
+    """W built once on rank ``src`` and replicated by a broadcast (north_star):
+    src: gb_clear + gb_store(msgs) + gb_seal; broadcast of its packed rows Wb; every other
+    rank: gb_clear + gb_or_bits(Wb) + gb_seal.  Only ``src`` reads ``msgs``."""
+    rank, ws = world()
+    if group is not None:
+        rank, ws = dist.get_rank(group), dist.get_world_size(group)
+    net.clear(stream)
+    if rank == src and msgs is not None and msgs.shape[0]:
+        net.store(msgs, stream)
+    if ws == 1:
+        net.seal(stream, check=False)
+        return
+    if rank == src:
+        net.seal(stream, check=False)
+        wb = net.bits()
+    else:
+        wb = torch.empty((net.n_padded, net.nw), dtype=torch.int32, device=f"cuda:{net.device}")
+    broadcast_(wb, src, group)
+    if rank != src:
+        net.or_bits(wb.unsqueeze(0), stream)
+        net.seal(stream, check=False)
 
 
 def max_over_ranks(values, device=None):
@@ -78,12 +130,32 @@ def sum_over_ranks(values, device=None):
 
 
 def sharded_store(net, msgs_shard, group=None, stream=None):
-    """gb_clear + gb_store(shard) + MAX merge + gb_seal on one rank."""
+    """gb_clear + gb_store(shard) + MAX merge + gb_seal on one rank (no host sync: the
+    outcome is checked by seal_status_all)."""
     net.clear(stream)
     if msgs_shard.shape[0]:
         net.store(msgs_shard, stream)
     merge_weights_(net.weights(), group)
-    net.seal(stream)
+    net.seal(stream, check=False)
+
+
+def seal_status_all(net, group=None):
+    """gb_seal_status on every rank, agreed over the group: if any rank's seal failed
+    (broken invariants, or its shard held messages with invalid symbols) every rank
+    raises, so no rank is left waiting in a later collective."""
+    from . import GBError
+    err = None
+    try:
+        net.seal_status()
+    except GBError as e:
+        err = e
+    if not (dist.is_available() and dist.is_initialized()):
+        if err:
+            raise err
+        return
+    bad = sum_over_ranks([1 if err else 0], device=f"cuda:{net.device}" if _is_nccl(group) else None)[0]
+    if bad:
+        raise err if err else GBError(-1, f"gb_seal failed on {bad} other rank(s)")
 
 
 def gather_bits(wb: torch.Tensor, group=None) -> torch.Tensor:
@@ -102,14 +174,46 @@ def gather_bits(wb: torch.Tensor, group=None) -> torch.Tensor:
     return out.to(wb.device)
 
 
-def sharded_store_bits(net, msgs_shard, group=None, stream=None):
-    """gb_clear + gb_store(shard) + gb_seal (pack the partial) + all-gather of
-    the packed partials + gb_or_bits + gb_seal on one rank (N3 merge)."""
+def gather_(t: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather a 1-D tensor into [G, n] (NCCL on the device; gloo via host)."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return t.unsqueeze(0).contiguous()
+    ws = dist.get_world_size(group)
+    if _is_nccl(group):
+        out = torch.empty((ws,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(out, t.contiguous(), group=group)
+        return out
+    src = t.detach().cpu().contiguous()
+    out = torch.empty((ws,) + tuple(src.shape), dtype=src.dtype)
+    dist.all_gather(list(out.unbind(0)), src, group=group)
+    return out.to(t.device)
+
+
+def sharded_store_upper(net, msgs_shard, group=None, stream=None):
+    """N3 merge with the upper triangle only (W symmetric): gb_clear +
+    gb_store(shard) + gb_seal, gb_pack_upper (C(C-1)/2 of the C^2 cluster-pair blocks),
+    all-gather, gb_or_upper (ORs each block and its mirror into W8) + gb_seal."""
     net.clear(stream)
     if msgs_shard.shape[0]:
         net.store(msgs_shard, stream)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        net.seal(stream)
+        net.seal(stream, check=False)
+        allu = gather_(net.pack_upper(stream=stream), group)
+        net.clear(stream)
+        net.or_upper(allu, stream)
+    net.seal(stream, check=False)
+
+
+def sharded_store_bits(net, msgs_shard, group=None, stream=None):
+    """gb_clear + gb_store(shard) + gb_seal (pack the partial) + all-gather of
+    the packed partials + gb_or_bits + gb_seal on one rank (N3 merge).  The seals
+    do not synchronise the host; the invalid-message count of the shard stays on the
+    device until seal_status_all (no rank raises before the collective)."""
+    net.clear(stream)
+    if msgs_shard.shape[0]:
+        net.store(msgs_shard, stream)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        net.seal(stream, check=False)
         allb = gather_bits(net.bits(), group)
         net.or_bits(allb, stream)
-    net.seal(stream)
+    net.seal(stream, check=False)

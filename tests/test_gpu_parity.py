@@ -79,22 +79,18 @@ def test_store_matches_oracle(gb, c, l, m):
 @pytest.mark.parametrize("c,l,m", [(8, 128, 20000), (16, 512, 60000), (5, 33, 5000), (64, 32, 3000),
                                    (3, 100, 5000), (16, 256, 300000)])
 @pytest.mark.parametrize("path", ["privatised", "scatter"])
-def test_store_paths_match_oracle(gb, monkeypatch, c, l, m, path):
+def test_store_paths_match_oracle(gb, c, l, m, path):
     """Both store kernels (shared-memory bit tiles + apply pass for large
-    batches; scattered byte stores, forced with GB_STORE_SCATTER) give the
+    batches; scattered byte stores, forced with GB_OPT_STORE_SCATTER) give the
     oracle's W (Eq.(1)) byte for byte, accumulate over calls (OR),
     and skip + count messages holding a symbol >= L (reading R21)."""
-    if path == "scatter":
-        monkeypatch.setenv("GB_STORE_SCATTER", "1")
-    else:
-        monkeypatch.delenv("GB_STORE_SCATTER", raising=False)
     msgs = gbgen.messages(77 + m + c, m, c, l)
     bad = msgs[:5].copy()
     bad[0, c - 1] = l
     bad[1, 0] = 0xFFFF
     bad[2, c // 2] = 0xFFFE
     allm = np.concatenate([msgs[: m // 3], bad[:3], msgs[m // 3:]])
-    net = gb.Net(c, l)
+    net = gb.Net(c, l, store_scatter=int(path == "scatter"))
     net.store(to_dev(allm[: len(allm) // 2]))
     net.store(to_dev(allm[len(allm) // 2:]))
     with pytest.raises(gb.GBError) as ei:
@@ -156,9 +152,9 @@ def test_seal_invariants_every_tile(gb, c, l):
 
 @pytest.mark.parametrize("l,m,k", [(128, 20000, 3001), (100, 5000, 777), (97, 12000, 31), (128, 0, 64),
                                    (128, 30000, 1)])
-def test_hyb8_matches_oracle_and_generic(gb, monkeypatch, l, m, k):
+def test_hyb8_matches_oracle_and_generic(gb, l, m, k):
     """The C=8 hybrid kernel (staged push, TMA-stored output) against the
-    oracle and against the generic shared-memory kernel (GB_NO_HYB8): ragged
+    oracle and against the generic shared-memory kernel (GB_OPT_HYB8 = 0): ragged
     batch (k not a multiple of 32, k < 32), every erasure count 0..8 (e > 4
     goes to the wide-slot kernel), invalid probes, random non-stored probes."""
     c = 8
@@ -180,15 +176,15 @@ def test_hyb8_matches_oracle_and_generic(gb, monkeypatch, l, m, k):
     want = oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=20)
     got = gpu_decode(net, pr, 2, 1, 20)
     assert_same(got, want, 2, f"hyb8 l={l} m={m} k={k}")
-    monkeypatch.setenv("GB_NO_HYB8", "1")
+    net.set_option("hyb8", 0)
+    assert net.decode_kernel(2) == "decode_smem_kernel"
     assert_same(gpu_decode(net, pr, 2, 1, 20), want, 2, "generic")
     assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "T=3")
-    monkeypatch.delenv("GB_NO_HYB8")
+    net.set_option("hyb8", 1)
     assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "hyb8 T=3")
-    for split in ("0", "1"):                        # stage 2 whole / in two halves (density heuristic forced)
-        monkeypatch.setenv("GB_HYB8_SPLIT2", split)
+    for split in (0, 1):                            # stage 2 whole / in two halves (density heuristic forced)
+        net.set_option("hyb8_split", split)
         assert_same(gpu_decode(net, pr, 2, 1, 20), want, 2, f"hyb8 split2={split}")
-    monkeypatch.delenv("GB_HYB8_SPLIT2")
     net.close()
 
 
@@ -204,12 +200,12 @@ def test_or_bits_merge_equals_single(gb):
         fresh = gb.Net(c, l)
         fresh.or_bits(stacked)
         fresh.seal()
-        assert torch.equal(fresh.weights(), whole.weights())
+        assert torch.equal(fresh.weights_view(), whole.weights_view())
         assert torch.equal(fresh.bits(), whole.bits())
         # OR into a net that already holds a shard (accumulates)
         parts[0].or_bits(stacked[1:].contiguous())
         parts[0].seal()
-        assert torch.equal(parts[0].weights(), whole.weights())
+        assert torch.equal(parts[0].weights_view(), whole.weights_view())
         for n in parts + [whole, fresh]:
             n.close()
     net = gb.Net(4, 16)
@@ -231,8 +227,9 @@ def test_sharded_store_max_merge_equals_single(gb):
     msgs = gbgen.messages(5, m, c, l)
     whole = make_net(gb, msgs, c, l)
     parts = [make_net(gb, msgs[i::3], c, l) for i in range(3)]
-    merged = torch.maximum(torch.maximum(parts[0].weights(), parts[1].weights()), parts[2].weights())
-    assert torch.equal(merged, whole.weights())
+    merged = torch.maximum(torch.maximum(parts[0].weights_view(), parts[1].weights_view()),
+                           parts[2].weights_view())
+    assert torch.equal(merged, whole.weights_view())
     w8 = parts[0].weights()
     w8.copy_(merged)
     parts[0].seal()
@@ -448,10 +445,12 @@ def test_determinism(gb):
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
     (tensor-core SOS, shared-memory bit kernel, generic warp kernel).  SOS at
-    n_padded <= 1024 runs on a CTA pair (sos_tc2x2_kernel) unless GB_SOS_2CTA=0."""
-    if want in ("sos_tc2_kernel", "sos_tc3_kernel") and os.environ.get("GB_SOS_2CTA", "1") != "0":
-        want = want.replace("_kernel", "x2_kernel")
+    n_padded <= 4096 runs on a CTA pair (sos_tc2x2 / sos_tc3x2) unless
+    GB_OPT_SOS_PAIR = 0."""
     net = gb.Net(c, l)
+    if want in ("sos_tc2_kernel", "sos_tc3_kernel"):
+        assert net.decode_kernel(rule) == want.replace("_kernel", "x2_kernel")
+        net.set_option("sos_pair", 0)
     assert net.decode_kernel(rule) == want
 
 
@@ -562,7 +561,7 @@ def test_mixed_erasures_narrow_and_wide_slots(gb):
                                            (7, 100, 1500, 3, 1), (8, 96, 3000, 5, 4), (2, 1, 1, 1, 1),
                                            (8, 128, 8000, 4, 31743), (8, 128, 8000, 4, 31744),
                                            (4, 64, 500, 2, 40000)])
-def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
+def test_sos_pair_vs_single_cta(gb, c, l, m, e, gamma):
     """The CTA-pair SOS kernel (tcgen05 cta_group::2, M = 256, each CTA stages half
     of W's rows) and the single-CTA kernel give identical results, and both equal
     the oracle: the pair only re-tiles the exact int32 contraction of Eq.(10)-(11).
@@ -573,7 +572,7 @@ def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
     pr, _ = gbgen.probes(501 + c, msgs, 1537, e, l, random_count=5)
     res = {}
     for flag in ("1", "0"):
-        monkeypatch.setenv("GB_SOS_2CTA", flag)
+        net.set_option("sos_pair", int(flag))
         res[flag] = gpu_decode(net, pr, 0, gamma, 20)
         assert net.decode_kernel(0) == ("sos_tc2x2_kernel" if flag == "1" else "sos_tc2_kernel")
     for x, y in zip(res["1"], res["0"]):
@@ -585,26 +584,25 @@ def test_sos_pair_vs_single_cta(gb, monkeypatch, c, l, m, e, gamma):
 @pytest.mark.parametrize("c,l,m,e,gamma,k", [(16, 256, 100000, 8, 2, 300), (32, 64, 3000, 16, 1, 700),
                                              (9, 256, 20000, 4, 0, 257), (5, 250, 4000, 2, 300, 129),
                                              (16, 256, 30000, 8, 255, 200)])
-def test_sos_streamed_a_vs_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
+def test_sos_streamed_a_vs_oracle(gb, c, l, m, e, gamma, k):
     """The streamed-A SOS kernel (1024 < n_p <= 4096: A producer warps expand the
     state into a ring of swizzled stages, TMA ring of W8 + gamma*I) equals the
-    oracle and the 4-warp sos_tc_kernel (GB_SOS_TC3=0) bit for bit: ragged tiles,
+    oracle and the 4-warp sos_tc_kernel (GB_OPT_SOS_STREAMED = 0) bit for bit: ragged tiles,
     gamma = 0, gamma folded into B (<= 255) and added in the epilogue (300)."""
     msgs = gbgen.messages(600 + c + l, m, c, l)
     net = make_net(gb, msgs, c, l)
     pr, _ = gbgen.probes(601 + c, msgs, k, e, l, random_count=k // 10)
     pr[3, 0] = l                       # invalid symbol
-    monkeypatch.delenv("GB_SOS_TC3", raising=False)
     w8, _ = oracle.store(msgs, c, l)
     want = oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20)
     for flag, name in (("1", "sos_tc3x2_kernel"), ("0", "sos_tc3_kernel")):   # CTA pair / single CTA
-        monkeypatch.setenv("GB_SOS_2CTA", flag)
+        net.set_option("sos_pair", int(flag))
         assert net.decode_kernel(0) == name
         got = gpu_decode(net, pr, 0, gamma, 20)
         assert_same(got, want, 0, name)
         assert_same(gpu_decode(net, pr, 0, gamma, 3),
                     oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=3), 0, name + " T=3")
-    monkeypatch.setenv("GB_SOS_TC3", "0")
+    net.set_option("sos_streamed", 0)
     assert net.decode_kernel(0) == "sos_tc_kernel"
     other = gpu_decode(net, pr, 0, gamma, 20)
     for x, y in zip(got, other):
@@ -615,9 +613,9 @@ def test_sos_streamed_a_vs_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
 @pytest.mark.parametrize("c,l,m,e,k", [(16, 256, 100000, 8, 300), (16, 256, 20000, 11, 200), (12, 100, 3000, 5, 257),
                                        (16, 512, 50000, 7, 100), (9, 128, 8000, 3, 129), (16, 200, 0, 6, 64)])
 @pytest.mark.parametrize("rule", [1, 2])
-def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule):
+def test_l2t_matches_oracle_and_warp_kernel(gb, c, l, m, e, k, rule):
     """The thread-per-probe L2 kernel (staged push from L2-resident bit rows) against
-    the oracle and against the warp-per-probe decode_l2_kernel (GB_NO_L2T): mixed
+    the oracle and against the warp-per-probe decode_l2_kernel (GB_OPT_L2T = 0): mixed
     erasure counts (probes with more erased clusters than its 8 hybrid slots are
     queued to the warp kernel), ragged L, M=0, invalid probes, random probes.
     """
@@ -636,30 +634,28 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, monkeypatch, c, l, m, e, k, rule
     want = oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=20)
     assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, f"l2t c={c} l={l}")
     assert_same(gpu_decode(net, pr, rule, 1, 2), oracle.decode(w, c, l, pr, rule, gamma=1, max_iters=2), rule, "T=2")
-    monkeypatch.setenv("GB_NO_L2T", "1")
+    net.set_option("l2t", 0)
     assert_same(gpu_decode(net, pr, rule, 1, 20), want, rule, "warp kernel")
     net.close()
 
 
-@pytest.mark.parametrize("c,l,m,e,k,gamma,env,kernel", [
+@pytest.mark.parametrize("c,l,m,e,k,gamma,opts,kernel", [
     (3, 3, 4, 2, 1, 1, {}, "sos_tc2x2_kernel"),                        # §V-A: v^3 == v^1
     (5, 6, 25, 3, 300, 0, {}, "sos_tc2x2_kernel"),
-    (5, 6, 25, 3, 300, 0, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
+    (5, 6, 25, 3, 300, 0, {"sos_pair": 0}, "sos_tc2_kernel"),
     (8, 128, 30000, 5, 1000, 1, {}, "sos_tc2x2_kernel"),
-    (8, 128, 20000, 4, 1000, 2, {"GB_SOS_2CTA": "0"}, "sos_tc2_kernel"),
+    (8, 128, 20000, 4, 1000, 2, {"sos_pair": 0}, "sos_tc2_kernel"),
     (16, 256, 100000, 10, 300, 0, {}, "sos_tc3x2_kernel"),
-    (16, 256, 100000, 10, 300, 0, {"GB_SOS_2CTA": "0"}, "sos_tc3_kernel"),
-    (16, 256, 100000, 10, 300, 0, {"GB_SOS_TC3": "0"}, "sos_tc_kernel"),
+    (16, 256, 100000, 10, 300, 0, {"sos_pair": 0}, "sos_tc3_kernel"),
+    (16, 256, 100000, 10, 300, 0, {"sos_streamed": 0}, "sos_tc_kernel"),
     (8, 512, 30000, 5, 200, 0, {}, "sos_tc_kernel"),
     (4, 600, 3000, 2, 100, 0, {}, "decode_generic_kernel"),
 ])
-def test_sos_cycle_exit_flag(gb, monkeypatch, c, l, m, e, k, gamma, env, kernel):
+def test_sos_cycle_exit_flag(gb, c, l, m, e, k, gamma, opts, kernel):
     """GB_FLAG_CYCLE_EXIT: every sum-of-sum kernel stops a probe at
     the first round r >= 2 with V^r == V^{r-2} != V^{r-1}, status GB_CYCLE, state
     V^r -- bit-exact vs the oracle with the same flag; without the flag nothing
     changes; the flag leaves sum-of-max / hybrid untouched."""
-    for kk, v in env.items():
-        monkeypatch.setenv(kk, v)
     if m == 4:
         msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
         pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
@@ -668,6 +664,8 @@ def test_sos_cycle_exit_flag(gb, monkeypatch, c, l, m, e, k, gamma, env, kernel)
         pr, _ = gbgen.probes(801 + c, msgs, k, e, l, random_count=k // 3)
     w, _ = oracle.store(msgs, c, l)
     net = make_net(gb, msgs, c, l)
+    for kk, v in opts.items():
+        net.set_option(kk, v)
     assert net.decode_kernel(0) == kernel
     for T in (20, 7):
         want = oracle.decode(w, c, l, pr, 0, gamma=gamma, max_iters=T, flags=oracle.CYCLE_EXIT)
@@ -692,11 +690,10 @@ def test_sos_cycle_exit_flag(gb, monkeypatch, c, l, m, e, k, gamma, env, kernel)
 @pytest.mark.parametrize("c,l,m,e,k", [(8, 128, 5000, 4, 1000), (8, 128, 20000, 4, 700), (4, 16, 50, 2, 1000),
                                        (3, 3, 4, 2, 1), (5, 60, 2000, 3, 300), (16, 64, 3000, 9, 257),
                                        (7, 100, 0, 3, 64)])
-def test_som_tensor_core_matches_oracle(gb, monkeypatch, c, l, m, e, k):
+def test_som_tensor_core_matches_oracle(gb, c, l, m, e, k):
     """N2: sum-of-max as C exact per-source-cluster int8 contractions on the tensor
     cores (hit = count > 0, Eq.(6)-(7)) equals the oracle and the bit kernel bit for
     bit: states, rounds, statuses; ragged L, C=16, M=0, the §V-A example, T=2."""
-    monkeypatch.setenv("GB_SOM_TC", "1")
     if m == 4:
         msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
         pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
@@ -706,11 +703,12 @@ def test_som_tensor_core_matches_oracle(gb, monkeypatch, c, l, m, e, k):
         pr[2, 0] = l
     w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
     net = make_net(gb, msgs, c, l)
+    net.set_option("som_tensor", 1)
     assert net.decode_kernel(1) == "som_tc_kernel"
     for T in (20, 2):
         want = oracle.decode(w, c, l, pr, 1, gamma=1, max_iters=T)
         assert_same(gpu_decode(net, pr, 1, 1, T), want, 1, f"som_tc T={T}")
-    monkeypatch.delenv("GB_SOM_TC")
+    net.set_option("som_tensor", 0)
     assert net.decode_kernel(1) != "som_tc_kernel"
     assert_same(gpu_decode(net, pr, 1, 3, 20), oracle.decode(w, c, l, pr, 1, gamma=3, max_iters=20), 1, "bit")
     net.close()
@@ -780,33 +778,3 @@ def test_random_shapes_mixed_erasures_fuzz(gb, seed):
         assert_same(got, want, rule, f"mixed fuzz c={c} l={l} m={m} k={k} rule={rule} g={gamma} T={T} f={flags} "
                                      f"kernel={net.decode_kernel(rule)}")
         net.close()
-
-
-@pytest.mark.parametrize("c,l,m,e,gamma,k", [(8, 128, 5000, 4, 2, 1000), (8, 128, 30000, 5, 1, 700),
-                                             (4, 16, 50, 2, 6, 300), (3, 3, 4, 2, 1, 1), (5, 60, 2000, 3, 0, 257),
-                                             (7, 100, 3000, 3, 4, 129), (16, 64, 3000, 9, 3, 200)])
-def test_sos_fp4_matches_oracle(gb, monkeypatch, c, l, m, e, gamma, k):
-    """Sum-of-sum on block-scaled FP4 tensor cores (kind::mxf4, opt-in GB_SOS_FP4=1):
-    V, W in {0, 1} and gamma in {0, 1, 2, 3, 4, 6} are e2m1 values, so with unit
-    scales the fp32 sums are the exact integer scores -- bit-exact vs the oracle
-    (states, rounds, statuses), also with the cycle-exit flag; ragged L and
-    n_p not a multiple of the 256-neuron K block."""
-    monkeypatch.setenv("GB_SOS_FP4", "1")
-    if m == 4:
-        msgs = np.array([[0, 0, 0], [1, 1, 0], [2, 1, 0], [0, 2, 0]], np.uint16)
-        pr = np.array([[0xFFFF, 0xFFFF, 0]], np.uint16)
-    else:
-        msgs = gbgen.messages(1100 + c + l, m, c, l)
-        pr, _ = gbgen.probes(1101 + c, msgs, k, e, l, random_count=k // 5)
-        pr[0, 0] = l
-    w, _ = oracle.store(msgs, c, l)
-    net = make_net(gb, msgs, c, l)
-    if gamma == 2:
-        assert net.decode_kernel(0) == "sos_fp4_kernel"
-    for T in (20, 3):
-        assert_same(gpu_decode(net, pr, 0, gamma, T), oracle.decode(w, c, l, pr, 0, gamma, T), 0, f"fp4 T={T}")
-    st, it, ss = net.decode(to_dev(pr), 0, gamma=gamma, max_iters=20, flags=gb.FLAG_CYCLE_EXIT)
-    torch.cuda.synchronize()
-    got = (st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy())
-    assert_same(got, oracle.decode(w, c, l, pr, 0, gamma, 20, flags=oracle.CYCLE_EXIT), 0, "fp4 cycle")
-    net.close()

@@ -2,9 +2,8 @@
 
 Covers every kernel family: store (scattered + privatised) + apply + seal, OR of packed
 partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l2 (list mode),
-SOS pair / streamed-A / 4-warp / generic / FP4, the cycle-exit flag, and the tensor-core SOM kernel.
+SOS pair / streamed-A / 4-warp / generic, the cycle-exit flag, and the tensor-core SOM kernel.
 """
-import os
 import sys
 import numpy as np
 import torch
@@ -28,22 +27,21 @@ for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 50
         net.decode(probes, rule, gamma=2, max_iters=6)
     net.decode(probes, 0, gamma=0, max_iters=6, flags=gb.FLAG_CYCLE_EXIT)
     if c == 8 and l == 128:
-        os.environ["GB_SOM_TC"] = "1"
+        net.set_option("som_tensor", 1)
         net.decode(probes, 1, gamma=1, max_iters=6)
-        del os.environ["GB_SOM_TC"]
-        os.environ["GB_SOS_FP4"] = "1"
-        net.decode(probes, 0, gamma=2, max_iters=6)
-        net.decode(probes, 0, gamma=0, max_iters=6, flags=gb.FLAG_CYCLE_EXIT)
-        del os.environ["GB_SOS_FP4"]
-        for split in ("0", "1"):
-            os.environ["GB_HYB8_SPLIT2"] = split
+        net.set_option("som_tensor", 0)
+        for split in (0, 1):
+            net.set_option("hyb8_split", split)
             net.decode(probes, 2, gamma=1, max_iters=6)
-        del os.environ["GB_HYB8_SPLIT2"]
+        net.set_option("hyb8_split", -1)
         part = gb.Net(c, l)
         part.store(torch.from_numpy(msgs[: m // 2].view(np.int16)).cuda())
         part.seal()
         fresh = gb.Net(c, l)
         fresh.or_bits(torch.stack([part.bits(), net.bits()]).contiguous())
+        fresh.seal()
+        fresh.clear()
+        fresh.or_upper(torch.stack([part.pack_upper(), net.pack_upper()]).contiguous())
         fresh.seal()
         part.close()
         fresh.close()
