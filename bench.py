@@ -360,6 +360,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=18.0)   # calibration on 256 probes overestimates the time (~0.7x measured)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="kernel-selection option NAME=VALUE for gb_set_option (A/B experiments)")
     ap.add_argument("--cpu-threads", type=int, default=None,
                     help="host threads of the cpu_baseline oracle (default: all cores; 1 for the C1 figure)")
     args = ap.parse_args()
@@ -400,7 +402,7 @@ def main():
     my_msgs = msgs if rank == 0 else msgs[:0]
     msgs_d = torch.from_numpy(np.ascontiguousarray(my_msgs).view(np.int16)).to(dev)
     probes_d = torch.from_numpy(probes.view(np.int16)).to(dev)
-    net = gb.Net(c, l, device=local)
+    net = gb.Net(c, l, device=local, **{kv.split("=")[0]: int(kv.split("=")[1]) for kv in args.opt})
     out = net.alloc_outputs(k, device=True)
     stream = torch.cuda.current_stream()
     nw = net.nw

@@ -39,6 +39,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     nvcc = os.environ.get("NVCC", "nvcc")
     os.makedirs(OBJ, exist_ok=True)
     extra = ["-Xptxas", "-v"] if verbose else []
+    # experiment builds for same-box A/B (tools/ab.sh): GB_NVCC_DEFINES="-DNAME=VALUE ..."
+    extra += os.environ.get("GB_NVCC_DEFINES", "").split()
 
     def one(src):
         obj = os.path.join(OBJ, os.path.basename(src)[:-3] + ".o")

@@ -39,6 +39,10 @@ namespace {
 // 1.18 vs 1.04 ms, C2 hybrid (10^7) 4.74 vs 3.33 ms: the register cap serialises the staged
 // loads, and each half box waits for the TMA unit to read the previous one.
 constexpr int kNT = 768;            // threads per CTA (one probe each)
+#ifndef GB_HYB8_S1X
+#define GB_HYB8_S1X 0
+#endif
+constexpr int kS1X = GB_HYB8_S1X;   // words whose second candidate row joins stage 1
 constexpr int kWarps = kNT / 32;
 constexpr int kRowB = 128;          // bytes per W bit row (8 clusters x 16 B)
 constexpr int kClusterB = 128 * kRowB;   // bytes of the 128 rows of one cluster
@@ -205,10 +209,10 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                 // block c_t of row (c2, 32u + b): rb + (32u + b) * 128
                                 const uint32_t rb = w_s + ((slots >> (4 * sidx)) & 15u) * kClusterB + (ct << 4);
                                 uint32_t h[4] = {0u, 0u, 0u, 0u};
-                                // stage 1: the lowest candidate of each non-empty word (all four
-                                // loads in flight together)
+                                // stage 1: the lowest candidate of each non-empty word (+ the
+                                // highest other candidate of words 0..kS1X-1); all loads in flight
                                 {
-                                    uint32_t r[4][4];
+                                    uint32_t r[4 + kS1X][4];
 #pragma unroll
                                     for (int u = 0; u < 4; ++u) {
                                         const uint32_t x = xr[sidx][u];
@@ -217,7 +221,20 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                         lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
                                     }
 #pragma unroll
-                                    for (int v = 0; v < 4; ++v) h[v] = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+                                    for (int u = 0; u < kS1X; ++u) {
+                                        const uint32_t x = xr[sidx][u];
+                                        const uint32_t x2 = x & (x - 1u);
+#pragma unroll
+                                        for (int v = 0; v < 4; ++v) r[4 + u][v] = 0u;
+                                        lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[4 + u]);
+                                    }
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) {
+                                        uint32_t o = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+#pragma unroll
+                                        for (int u = 0; u < kS1X; ++u) o |= r[4 + u][v];
+                                        h[v] = o;
+                                    }
                                 }
                                 uint32_t miss = 0u;
 #pragma unroll
@@ -226,19 +243,20 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                     // stage 2: the highest other candidate of each word holding >= 2
                                     // (dense W: words 0-1, a cover check, then words 2-3); the loads
                                     // of a group are predicated and in flight together
+                                    constexpr bool kSplit = SPLIT2 && kS1X == 0;
 #pragma unroll
-                                    for (int g = 0; g < (SPLIT2 ? 2 : 1); ++g) {
-                                        if (SPLIT2 && g == 1) {
+                                    for (int g = 0; g < (kSplit ? 2 : 1); ++g) {
+                                        if (kSplit && g == 1) {
                                             miss = 0u;
 #pragma unroll
                                             for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
                                             if (!miss) break;
                                         }
-                                        constexpr int kW = SPLIT2 ? 2 : 4;
-                                        uint32_t r[kW][4];
+                                        constexpr int kW = kSplit ? 2 : 4 - kS1X;
+                                        uint32_t r[kW > 0 ? kW : 1][4];
 #pragma unroll
                                         for (int uu = 0; uu < kW; ++uu) {
-                                            const int u = g * kW + uu;
+                                            const int u = kS1X + g * kW + uu;
                                             const uint32_t x = xr[sidx][u];
                                             const uint32_t x2 = x & (x - 1u);
 #pragma unroll

@@ -44,6 +44,26 @@ __device__ __forceinline__ void ldg_block(const uint32_t *p, uint32_t (&v)[WC]) 
     }
 }
 
+// Predicated 16-byte read-only load (v unchanged when p == 0): a stage's row loads issue back
+// to back without branches, so their L2 latencies overlap.
+__device__ __forceinline__ void ldg4p(uint32_t p, const uint32_t *a, uint32_t (&v)[4]) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %4, 0;\n\t@q ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%5];\n\t}"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+        : "r"(p), "l"(a));
+}
+
+template <int WC>
+__device__ __forceinline__ void ldg_blockp(uint32_t p, const uint32_t *a, uint32_t (&v)[WC]) {
+    static_assert(WC % 4 == 0, "predicated block loads need Wc % 4 == 0");
+#pragma unroll
+    for (int q = 0; q < WC / 4; ++q) {
+        uint32_t t[4] = {0u, 0u, 0u, 0u};
+        ldg4p(p, a + 4 * q, t);
+        v[4 * q] = t[0]; v[4 * q + 1] = t[1]; v[4 * q + 2] = t[2]; v[4 * q + 3] = t[3];
+    }
+}
+
 template <int WC, int RULE, int MAXS, int NT>
 __global__ void __launch_bounds__(NT, 1)
 decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int T,
@@ -51,10 +71,12 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                   uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
                   unsigned long long *__restrict__ ovf_count, uint32_t *__restrict__ xscratch) {
     constexpr int LP = 32 * WC;
-    // rows per push stage: sum-of-max's first round covers whole erased clusters from
-    // all-ones sources, where wider stages pay (same-box A/B at C4: SOM 6 rows 2.02 ms vs
-    // 4 rows 2.31 ms; hybrid 4 rows 2.32 ms vs 6 rows 2.59 ms)
-    constexpr int kStage = RULE == GB_SUM_OF_MAX ? 6 : 4;
+    // rows per push stage = one word group of G words (the lowest remaining candidate of each),
+    // all G loads predicated and in flight together; groups are visited cyclically until the
+    // target is covered or the source exhausted.  Sum-of-max's first round covers whole erased
+    // clusters from all-ones sources, where wider stages pay.
+    constexpr int G = (RULE == GB_SUM_OF_MAX ? 8 : 4) < WC ? (RULE == GB_SUM_OF_MAX ? 8 : 4) : WC;
+    static_assert(WC % G == 0, "word groups tile the block");
     extern __shared__ uint32_t sm[];
     const int tid = threadIdx.x;
     const int C = s.C, nw = s.nw;
@@ -175,26 +197,31 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                         for (int u = 0; u < WC; ++u) h[u] = 0u;
                         uint32_t miss = 1u;
                         while (miss && left) {
-                            // one stage: the lowest remaining candidate of successive words, <= 4 rows
-                            int cnt = 0;
 #pragma unroll
-                            for (int u = 0; u < WC; ++u) {
-                                if (rem[u] && cnt < kStage) {
-                                    const uint32_t b = __ffs(rem[u]) - 1;
-                                    rem[u] &= rem[u] - 1u;
-                                    ++cnt;
-                                    uint32_t r[WC];
-                                    ldg_block<WC>(base + (size_t)(u * 32 + b) * nw, r);
+                            for (int grp = 0; grp < WC / G; ++grp) {
+                                if (!(miss && left)) break;
+                                // one stage: the lowest remaining candidate of each word of the group
+                                uint32_t r[G][WC];
 #pragma unroll
-                                    for (int v = 0; v < WC; ++v) h[v] |= r[v];
+                                for (int q = 0; q < G; ++q) {
+                                    const int u = grp * G + q;
+                                    const uint32_t x = rem[u];
+                                    rem[u] = x & (x - 1u);
+#pragma unroll
+                                    for (int v = 0; v < WC; ++v) r[q][v] = 0u;
+                                    ldg_blockp<WC>(x, base + (size_t)(u * 32 + __ffs(x) - 1) * nw, r[q]);
                                 }
-                            }
-                            miss = 0u;
-                            left = 0u;
+                                miss = 0u;
+                                left = 0u;
 #pragma unroll
-                            for (int u = 0; u < WC; ++u) {
-                                miss |= alive[u] & ~h[u];
-                                left |= rem[u];
+                                for (int v = 0; v < WC; ++v) {
+                                    uint32_t o = 0u;
+#pragma unroll
+                                    for (int q = 0; q < G; ++q) o |= r[q][v];
+                                    h[v] |= o;
+                                    miss |= alive[v] & ~h[v];
+                                    left |= rem[v];
+                                }
                             }
                         }
                         any = 0u;
