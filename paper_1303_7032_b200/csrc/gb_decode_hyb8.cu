@@ -39,10 +39,7 @@ namespace {
 // 1.18 vs 1.04 ms, C2 hybrid (10^7) 4.74 vs 3.33 ms: the register cap serialises the staged
 // loads, and each half box waits for the TMA unit to read the previous one.
 constexpr int kNT = 768;            // threads per CTA (one probe each)
-#ifndef GB_HYB8_S1X
-#define GB_HYB8_S1X 0
-#endif
-constexpr int kS1X = GB_HYB8_S1X;   // words whose second candidate row joins stage 1
+
 constexpr int kWarps = kNT / 32;
 constexpr int kRowB = 128;          // bytes per W bit row (8 clusters x 16 B)
 constexpr int kClusterB = 128 * kRowB;   // bytes of the 128 rows of one cluster
@@ -68,12 +65,22 @@ __device__ __forceinline__ void lds4p(uint32_t p, uint32_t a, uint32_t (&v)[4]) 
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
 
+// Two variants, chosen by W's density (seal counts the edges):
+//  SPLIT2 (dense W, density > 0.5): stage 1 = the lowest candidate of each word; stage 2 in two
+//    halves with a cover check between them (at C3 ~32 candidates per erased cluster, two more
+//    rows usually cover);
+//  sparse W: stage 1 also takes the highest other candidate of words 0-1 (few candidates: those
+//    loads are mostly predicated off, and the stage-2 branch is skipped more often).
+// Same-box A/B (round 2, predicated loads): C3 (density 0.70) 0.961 ms dense variant vs 1.066 with
+// the wider stage 1 (1.30 with all four words); C2 hybrid 10^7 (density 0.26) 2.24 ms wide vs
+// 2.37 narrow.
 template <bool SPLIT2>
 __global__ void __launch_bounds__(kNT, 1)
 decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
                    int T, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
                    uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
                    unsigned long long *__restrict__ ovf_count) {
+    constexpr int kS1X = SPLIT2 ? 0 : 2;   // words whose second candidate row joins stage 1
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
     const uint32_t w_s = sbase;

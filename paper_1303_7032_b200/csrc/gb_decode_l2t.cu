@@ -303,11 +303,13 @@ bool decode_l2t_supported(const gb_net *net, int rule) {
     const Shape &s = net->s;
     // measured (round 1, same box, next state in L2 scratch): faster than the warp-per-probe
     // kernel for the hybrid at C4 (2.59 vs 7.92 ms), Scenario 2 (0.270 vs 0.356 ms) and for
-    // sum-of-max at C4 (3.33 vs 4.59 ms); sum-of-max at Wc = 16 (16 slots x 64 B per thread)
-    // keeps decode_l2_kernel
+    // sum-of-max at C4 (3.33 vs 4.59 ms)
     if (net->opt[kOptL2t].load(std::memory_order_relaxed) == 0) return false;
     if (rule == GB_SUM_OF_SUM || s.C > kMaxC16) return false;
-    if (rule == GB_SUM_OF_MAX) return s.Wc == 4 || s.Wc == 8;
+    // sum-of-max at Wc = 16 (16 slots x 64 B per thread, 128 threads per SM) was left to the warp
+    // kernel while the stage loads were serial; with them in flight together it is faster
+    // (Scenario 2 sum-of-max 2.99 -> 1.74 ms, same-box A/B)
+    if (rule == GB_SUM_OF_MAX) return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;
     return s.Wc == 4 || s.Wc == 8 || s.Wc == 16;
 }
 
@@ -322,7 +324,7 @@ cudaError_t launch_decode_l2t(Call &cl, const uint16_t *probes, int64_t k, int r
         case 8: return h ? launch_t<8, GB_HYBRID, 8>(cl, probes, k, max_iters, state, iters, status)
                          : launch_t<8, GB_SUM_OF_MAX, 16>(cl, probes, k, max_iters, state, iters, status);
         default: return h ? launch_t<16, GB_HYBRID, 8>(cl, probes, k, max_iters, state, iters, status)
-                          : cudaErrorNotSupported;
+                          : launch_t<16, GB_SUM_OF_MAX, 16>(cl, probes, k, max_iters, state, iters, status);
     }
 }
 

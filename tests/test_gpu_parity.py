@@ -440,7 +440,7 @@ def test_determinism(gb):
                                            (16, 256, 1, "decode_l2t_kernel"), (16, 256, 2, "decode_l2t_kernel"),
                                            (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2t_kernel"),
                                            (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc_kernel"),
-                                           (16, 512, 2, "decode_l2t_kernel"), (16, 512, 1, "decode_l2_kernel"),
+                                           (16, 512, 2, "decode_l2t_kernel"), (16, 512, 1, "decode_l2t_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
     """The product path runs the intended sm_100a kernel for each shape/rule
