@@ -95,8 +95,10 @@ enum {
     GB_OPT_L2T = 4,            /* 1 (default): thread-per-probe L2 bit kernel; 0:
                                   warp-per-probe kernel (W rows beyond shared mem)   */
     GB_OPT_HYB8_SPLIT = 5,     /* -1 (default): choose the C = 8 hybrid kernel's
-                                  dense-W stage split by W's density (known once a
-                                  seal's status reached the host); 0 / 1 force it   */
+                                  push variant by W's density (known once a seal's
+                                  status reached the host): staged when dense (>0.65),
+                                  a uniform loop when sparse; 0 (loop) / 1 (staged)
+                                  force it (bit-exact either way)                   */
     GB_OPT_STORE_SCATTER = 6   /* 1: gb_store with scattered byte writes only;
                                   0 (default): shared-memory privatised tiles for
                                   large batches                                      */

@@ -6,16 +6,14 @@
 //
 //  * compile-time C / block size: no per-cluster predicates or runtime loops
 //    in ingest, prune and output;
-//  * the push of one (source -> target) pair reads candidate rows in stages
-//    instead of walking the source's bits one at a time:
-//      stage 1  the lowest candidate of every non-empty word of the source
-//               (up to 4 rows, addresses computed without a loop),
-//      stage 2  the highest candidate of every word holding >= 2 (for dense W
-//               in two halves, words 0-1 then 2-3, with a cover check between),
-//      stage 3  the remaining candidates, one at a time (the old walk);
-//    each stage runs only while some target candidate is still uncovered
-//    (bail-out-early), and every source candidate is visited by
-//    exactly one stage, so the cover H is the same OR of rows;
+//  * the push of one (source -> target) pair reads candidate rows several at a
+//    time instead of walking the source's bits one at a time: when W is dense
+//    in stages (the lowest candidate of every non-empty word of the source, then
+//    the highest other candidate of every word in two halves, then the rest one
+//    at a time), when sparse in a loop of "the lowest remaining candidate of
+//    every word"; each step runs only while some target candidate is still
+//    uncovered (bail-out-early), and every source candidate is read
+//    at most once, so the cover H is the same OR of rows;
 //  * output through a TMA tensor store: each warp writes its 32 probes'
 //    128-byte states into a 4 KiB shared-memory box in the 128-byte swizzle
 //    (16-byte chunk c of row r at chunk c ^ (r & 7): the lanes of a
@@ -65,22 +63,26 @@ __device__ __forceinline__ void lds4p(uint32_t p, uint32_t a, uint32_t (&v)[4]) 
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
 
-// Two variants, chosen by W's density (seal counts the edges):
-//  SPLIT2 (dense W, density > 0.5): stage 1 = the lowest candidate of each word; stage 2 in two
-//    halves with a cover check between them (at C3 ~32 candidates per erased cluster, two more
-//    rows usually cover);
-//  sparse W: stage 1 also takes the highest other candidate of words 0-1 (few candidates: those
-//    loads are mostly predicated off, and the stage-2 branch is skipped more often).
-// Same-box A/B (round 2, predicated loads): C3 (density 0.70) 0.961 ms dense variant vs 1.066 with
-// the wider stage 1 (1.30 with all four words); C2 hybrid 10^7 (density 0.26) 2.24 ms wide vs
-// 2.37 narrow.
-template <bool SPLIT2>
+// Two push variants, chosen by W's density (seal counts the edges):
+//  DENSE (density > 0.65): stage 1 = the lowest candidate row of each word of the source;
+//    stage 2 = the highest other candidate of each word, in two halves with a cover check
+//    between them (at C3 ~32 candidates per erased cluster: stage 1 covers ~77% of the pairs and
+//    two more rows usually cover the rest); stage 3 = the remaining rows one at a time;
+//  sparse: one loop whose every step reads the lowest remaining candidate row of each word (up to
+//    4 loads in flight) until the target is covered or the source exhausted -- few candidates per
+//    cluster, many of them dying, so the uniform loop wastes fewer warp slots than the stages.
+// Same-box A/B (round 2, 10^7 probes, hybrid, c=8 l=128): M=5k (density 0.26) 2.24 -> 1.74 ms
+// with the loop, M=10k (0.46) 4.11 -> 3.32, M=15k (0.60) 1.19 -> 1.08; the staged form stays
+// faster when dense: M=20k (C3, 0.70) 0.960 vs 0.973, M=30k (0.84) 0.855 vs 0.870.  A third form,
+// stage 1 then one "pull" row per uncovered target candidate (row i's block of the source meets
+// the source's remaining candidates, W symmetric), was slower at every density (C3 1.12 ms,
+// M=5k 2.11): its loads run on few lanes, so each costs almost a full wavefront.
+template <bool DENSE>
 __global__ void __launch_bounds__(kNT, 1)
 decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
                    int T, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
                    uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
                    unsigned long long *__restrict__ ovf_count) {
-    constexpr int kS1X = SPLIT2 ? 0 : 2;   // words whose second candidate row joins stage 1
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
     const uint32_t w_s = sbase;
@@ -216,86 +218,94 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                 // block c_t of row (c2, 32u + b): rb + (32u + b) * 128
                                 const uint32_t rb = w_s + ((slots >> (4 * sidx)) & 15u) * kClusterB + (ct << 4);
                                 uint32_t h[4] = {0u, 0u, 0u, 0u};
-                                // stage 1: the lowest candidate of each non-empty word (+ the
-                                // highest other candidate of words 0..kS1X-1); all loads in flight
-                                {
-                                    uint32_t r[4 + kS1X][4];
+                                if constexpr (!DENSE) {
+                                    // sparse: the lowest remaining candidate row of every word per
+                                    // step (4 loads in flight) until covered or exhausted
+                                    uint32_t rem[4];
 #pragma unroll
-                                    for (int u = 0; u < 4; ++u) {
-                                        const uint32_t x = xr[sidx][u];
+                                    for (int u = 0; u < 4; ++u) rem[u] = xr[sidx][u];
+                                    uint32_t miss;
+                                    do {
+                                        uint32_t r[4][4];
 #pragma unroll
-                                        for (int v = 0; v < 4; ++v) r[u][v] = 0u;
-                                        lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
-                                    }
+                                        for (int u = 0; u < 4; ++u) {
+                                            const uint32_t x = rem[u];
 #pragma unroll
-                                    for (int u = 0; u < kS1X; ++u) {
-                                        const uint32_t x = xr[sidx][u];
-                                        const uint32_t x2 = x & (x - 1u);
-#pragma unroll
-                                        for (int v = 0; v < 4; ++v) r[4 + u][v] = 0u;
-                                        lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[4 + u]);
-                                    }
-#pragma unroll
-                                    for (int v = 0; v < 4; ++v) {
-                                        uint32_t o = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
-#pragma unroll
-                                        for (int u = 0; u < kS1X; ++u) o |= r[4 + u][v];
-                                        h[v] = o;
-                                    }
-                                }
-                                uint32_t miss = 0u;
-#pragma unroll
-                                for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                if (miss) {
-                                    // stage 2: the highest other candidate of each word holding >= 2
-                                    // (dense W: words 0-1, a cover check, then words 2-3); the loads
-                                    // of a group are predicated and in flight together
-                                    constexpr bool kSplit = SPLIT2 && kS1X == 0;
-#pragma unroll
-                                    for (int g = 0; g < (kSplit ? 2 : 1); ++g) {
-                                        if (kSplit && g == 1) {
-                                            miss = 0u;
-#pragma unroll
-                                            for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                            if (!miss) break;
+                                            for (int v = 0; v < 4; ++v) r[u][v] = 0u;
+                                            lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
+                                            rem[u] = x & (x - 1u);
                                         }
-                                        constexpr int kW = kSplit ? 2 : 4 - kS1X;
-                                        uint32_t r[kW > 0 ? kW : 1][4];
+                                        miss = 0u;
 #pragma unroll
-                                        for (int uu = 0; uu < kW; ++uu) {
-                                            const int u = kS1X + g * kW + uu;
-                                            const uint32_t x = xr[sidx][u];
-                                            const uint32_t x2 = x & (x - 1u);
-#pragma unroll
-                                            for (int v = 0; v < 4; ++v) r[uu][v] = 0u;
-                                            lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[uu]);
+                                        for (int v = 0; v < 4; ++v) {
+                                            h[v] |= (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+                                            miss |= alive[v] & ~h[v];
                                         }
-#pragma unroll
-                                        for (int uu = 0; uu < kW; ++uu) {
-#pragma unroll
-                                            for (int v = 0; v < 4; ++v) h[v] |= r[uu][v];
-                                        }
-                                    }
-                                    miss = 0u;
-#pragma unroll
-                                    for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                    if (miss) {
-                                        // stage 3: the rest, one row at a time
+                                    } while (miss && ((rem[0] | rem[1]) | (rem[2] | rem[3])));
+                                } else {
+                                    // stage 1: the lowest candidate of each non-empty word, in flight
+                                    // together
+                                    {
+                                        uint32_t r[4][4];
 #pragma unroll
                                         for (int u = 0; u < 4; ++u) {
                                             const uint32_t x = xr[sidx][u];
-                                            uint32_t rem = x & (x - 1u);                      // minus stage 1
-                                            if (rem) rem &= ~(1u << highbit(rem));            // minus stage 2
-                                            while (rem && miss) {
-                                                const uint32_t b = lowbit(rem);
-                                                rem &= rem - 1u;
-                                                uint32_t r[4];
-                                                lds4(rb + (u * 32 + b) * kRowB, r);
+#pragma unroll
+                                            for (int v = 0; v < 4; ++v) r[u][v] = 0u;
+                                            lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
+                                        }
+#pragma unroll
+                                        for (int v = 0; v < 4; ++v) h[v] = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+                                    }
+                                    uint32_t miss = 0u;
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
+                                    if (miss) {
+                                        // stage 2: the highest other candidate of each word holding
+                                        // >= 2, words 0-1, a cover check, then words 2-3 (the loads of
+                                        // a half predicated and in flight together)
+#pragma unroll
+                                        for (int g = 0; g < 2; ++g) {
+                                            if (g == 1) {
                                                 miss = 0u;
 #pragma unroll
-                                                for (int v = 0; v < 4; ++v) {
-                                                    h[v] |= r[v];
-                                                    miss |= alive[v] & ~h[v];
+                                                for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
+                                                if (!miss) break;
+                                            }
+                                            uint32_t r[2][4];
+#pragma unroll
+                                            for (int uu = 0; uu < 2; ++uu) {
+                                                const int u = 2 * g + uu;
+                                                const uint32_t x = xr[sidx][u];
+                                                const uint32_t x2 = x & (x - 1u);
+#pragma unroll
+                                                for (int v = 0; v < 4; ++v) r[uu][v] = 0u;
+                                                lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[uu]);
+                                            }
+#pragma unroll
+                                            for (int v = 0; v < 4; ++v) h[v] |= r[0][v] | r[1][v];
+                                        }
+                                        miss = 0u;
+#pragma unroll
+                                        for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
+                                        if (miss) {
+                                            // stage 3: the rest, one row at a time
+#pragma unroll
+                                            for (int u = 0; u < 4; ++u) {
+                                                const uint32_t x = xr[sidx][u];
+                                                uint32_t rem = x & (x - 1u);                   // minus stage 1
+                                                if (rem) rem &= ~(1u << highbit(rem));         // minus stage 2
+                                                while (rem && miss) {
+                                                    const uint32_t b = lowbit(rem);
+                                                    rem &= rem - 1u;
+                                                    uint32_t r[4];
+                                                    lds4(rb + (u * 32 + b) * kRowB, r);
+                                                    miss = 0u;
+#pragma unroll
+                                                    for (int v = 0; v < 4; ++v) {
+                                                        h[v] |= r[v];
+                                                        miss |= alive[v] & ~h[v];
+                                                    }
                                                 }
                                             }
                                         }
@@ -413,12 +423,10 @@ cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int 
     // the output tensor map is a kernel parameter (copied at launch): encoded per call
     alignas(64) CUtensorMap map;
     if (!encode_out_map(state, k, &map)) return cudaErrorNotSupported;
-    // Stage 2 in two halves with a cover check between them pays when W is dense (most pairs
-    // reach stage 2 and two more rows usually cover): same-box A/B at C3 (density 0.70)
-    // 1.109 -> 1.053 ms, at C2 (density 0.26) 3.33 -> 3.59 ms.  GB_OPT_HYB8_SPLIT forces it.
+    // push variant by W's density (see the kernel's comment); GB_OPT_HYB8_SPLIT forces it
     const int fs = cl.opt(kOptHyb8Split);
-    const bool split2 = fs >= 0 ? (fs != 0) : (net->density.load(std::memory_order_relaxed) > 0.5);
-    auto fn = split2 ? decode_hyb8_kernel<true> : decode_hyb8_kernel<false>;   // compile-time: no cost when off
+    const bool dense = fs >= 0 ? (fs != 0) : (net->density.load(std::memory_order_relaxed) > 0.65);
+    auto fn = dense ? decode_hyb8_kernel<true> : decode_hyb8_kernel<false>;   // compile-time variants
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
     if (e != cudaSuccess) return e;
     int64_t grid = (k + kNT - 1) / kNT;

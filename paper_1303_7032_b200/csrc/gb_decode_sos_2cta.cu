@@ -108,8 +108,17 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     bool active = false;
     uint32_t dirty = (nkb * 4 >= 32) ? 0xffffffffu : ((1u << (nkb * 4)) - 1u);
     uint32_t nzcur = 0u;
+    // The next probe is taken in two steps so neither waits at the round boundary: its
+    // queue index when a slot is refilled (fetch), its symbols at the start of the next
+    // round's epilogue, where the loads overlap that round's MMAs (fetch_syms).
+    bool qready = false;
     auto fetch = [&]() {
         pn = (int64_t)atomicAdd(queue, 1ull);
+        qready = false;
+    };
+    auto fetch_syms = [&]() {
+        if (qready) return;
+        qready = true;
         if (pack && pn < k) {
             uint32_t w4[4] = {0u, 0u, 0u, 0u};
             const uint16_t *pr = probes + pn * s.C;
@@ -121,6 +130,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     };
     auto refill = [&]() {
         for (;;) {
+            fetch_syms();
             p = pn;
             const uint4 q = qn;
             fetch();
@@ -245,6 +255,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         } else {
             // ---- epilogue: per-cluster max + mask of each pass (a4)
             const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+            fetch_syms();
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
                 const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
                 const uint32_t buf = pc_e & 1u;

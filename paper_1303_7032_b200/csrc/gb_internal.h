@@ -146,7 +146,7 @@ enum : int {
     kOptSomTensor = 2,     // exact sum-of-max on the tensor cores (N2)
     kOptHyb8 = 3,          // C = 8 hybrid kernel
     kOptL2t = 4,           // thread-per-probe L2 bit kernel
-    kOptHyb8Split = 5,     // dense-W stage split of the C = 8 hybrid kernel: -1 auto, 0, 1
+    kOptHyb8Split = 5,     // push variant of the C = 8 hybrid kernel: -1 by density, 0 loop, 1 staged
     kOptStoreScatter = 6,  // store with scattered byte writes only (no privatised tiles)
 };
 int option_default(int o);
