@@ -62,7 +62,6 @@ __device__ __forceinline__ void lds4p(uint32_t p, uint32_t a, uint32_t (&v)[4]) 
 }
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
 __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
-
 // Two push variants, chosen by W's density (seal counts the edges):
 //  DENSE (density > 0.65): stage 1 = the lowest candidate row of each word of the source;
 //    stage 2 = the highest other candidate of each word, in two halves with a cover check
@@ -77,6 +76,18 @@ __device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); 
 // stage 1 then one "pull" row per uncovered target candidate (row i's block of the source meets
 // the source's remaining candidates, W symmetric), was slower at every density (C3 1.12 ms,
 // M=5k 2.11): its loads run on few lanes, so each costs almost a full wavefront.
+//
+// The kernel is bound by the LSU data pipe (~87% of one shared-memory wavefront per SM per clock
+// at C3); half of its wavefronts are bank conflicts, because a row block sits in the bank group of
+// its target cluster and the 8 lanes of a quarter-warp target random clusters.  Measured and not
+// kept (round 2, same-box A/B at C3):
+//  * unpredicated stage loads (empty words read a discarded row, fixed up in a rare branch):
+//    11% fewer instructions, ALU pipe 71% -> 55%, but 0.961 vs 0.931 ms -- not ALU-bound;
+//  * a conflict-free probe order: each CTA classifies its 768-probe chunk by erasure set and
+//    places 4 probes erasing E and 4 erasing ~E on every quarter-warp (counting sort in shared
+//    memory, CTA-wide staging of the output rows): conflicts 118M -> 51M per launch, but 1.15 ms
+//    (three CTA barriers per chunk and the exposed probe loads: long-scoreboard and barrier
+//    stalls).  Host-side ordering of the same probes (no in-kernel cost) gives 0.88 vs 0.97 ms.
 template <bool DENSE>
 __global__ void __launch_bounds__(kNT, 1)
 decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
@@ -87,7 +98,7 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
     const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
     const uint32_t w_s = sbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t stg = sbase + 1024 * kRowB + warp * kStageB;
+    const uint32_t stg = w_s + 1024 * kRowB + warp * kStageB;
     const uint32_t my_row = stg + (lane & (kBoxRows - 1)) * 128;
     const uint32_t sw = (uint32_t)(lane & 7);
 
@@ -163,14 +174,17 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                 sp_lo |= (uint64_t)sym[c] << (16 * c);
                 sp_hi |= (uint64_t)sym[c + 4] << (16 * c);
             }
-#pragma unroll
-            for (int kk = 0; kk < 8; ++kk) {
+            auto next_row = [&]() {   // row address of the next known cluster
                 const uint32_t kc = km ? (uint32_t)(__ffs(km) - 1) : 0u;
                 km &= km - 1u;
                 const uint32_t sk = (uint32_t)(((kc < 4) ? sp_lo : sp_hi) >> (16 * (kc & 3))) & 0xffffu;
-                ra[kk] = w_s + kc * kClusterB + sk * kRowB;
-            }
+                return w_s + kc * kClusterB + sk * kRowB;
+            };
             const uint32_t nk = 8u - nslot;
+            // e <= 4 here, so at least 4 known clusters: their rows unconditionally, the others
+            // (e < 4) in a second pass (same-box A/B: C3 0.962 -> 0.931 ms, M=30k 0.856 -> 0.830)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) ra[kk] = next_row();
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
 #pragma unroll
@@ -180,12 +194,29 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
 #pragma unroll
                     for (int u = 0; u < 4; ++u) xr[t][u] = rmask[u];
 #pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        if (kk < (int)nk) {
-                            uint32_t r[4];
-                            lds4(ra[kk] + (ct << 4), r);
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint32_t r[4];
+                        lds4(ra[kk] + (ct << 4), r);
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) xr[t][u] &= r[u];
+                        for (int u = 0; u < 4; ++u) xr[t][u] &= r[u];
+                    }
+                }
+            }
+            if (work && nk > 4) {
+#pragma unroll
+                for (int kk = 4; kk < 8; ++kk) ra[kk] = next_row();
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (t < (int)nslot) {
+                        const uint32_t ct = (slots >> (4 * t)) & 15u;
+#pragma unroll
+                        for (int kk = 4; kk < 8; ++kk) {
+                            if (kk < (int)nk) {
+                                uint32_t r[4];
+                                lds4(ra[kk] + (ct << 4), r);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) xr[t][u] &= r[u];
+                            }
                         }
                     }
                 }
