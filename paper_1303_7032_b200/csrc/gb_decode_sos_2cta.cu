@@ -23,6 +23,7 @@
 // barriers; the pair keeps iterating while either CTA has an active slot.
 #include <cuda.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -128,14 +129,17 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             qn = make_uint4(w4[0], w4[1], w4[2], w4[3]);
         }
     };
-    auto refill = [&]() {
+    // refill: zmask = the words of the slot's state that may be nonzero (all at the start, else
+    // the nonzero words of the finished probe's state)
+    auto refill = [&](uint32_t zmask) {
         for (;;) {
             fetch_syms();
             p = pn;
             const uint4 q = qn;
             fetch();
             uint32_t *Vc = Vs + par * nw * kTM;
-            for (int w = 0; w < nw; ++w) Vc[w * kTM + m] = 0u;
+            for (uint32_t d = zmask; d; d &= d - 1u) Vc[(__ffs(d) - 1) * kTM + m] = 0u;
+            zmask = 0u;
             rl = 0;
             if (p >= k) { active = false; return; }
             auto sym_of = [&](int c) -> unsigned {
@@ -183,10 +187,37 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             tma_load_2d_pair(Bs + r0 * kKB, &wmap, full_leader0 + 8u * st, kb * kKB, n0 + (int)rank * half + r0);
         ++it_p;
     };
+    // A finished probe's state (in the Vn area, untouched until the next round's epilogue) is
+    // stored at the start of that epilogue, while the tensor cores run the round's first pass,
+    // instead of at the round boundary, and a refill zeroes only the words the finished state had
+    // set.  Round boundary at C2 (clock64 trace of CTA 0, GB_SOS_TRACE builds): last pass's
+    // epilogue 1.7k cycles, convergence + output + refill 3.4k -> 2.4k, A update 2.2k, cluster
+    // barrier 0.6-3k, against 21.5k cycles of MMAs per round; C2 10^6 probes 2.72 -> 2.59 ms.
+    // Measured and not kept: the A update K block by K block with the next block's state words
+    // loaded ahead (5.4k cycles, 2.81 ms).
+    int64_t pend = -1;
+    auto flush = [&]() {
+        if (pend >= 0) {
+            uint32_t *out = out_state + pend * nw;
+            for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
+            pend = -1;
+        }
+    };
     if (epi) fetch();
-    if (epi) refill();
+    if (epi) refill(nw >= 32 ? 0xffffffffu : ((1u << nw) - 1u));
+#ifdef GB_SOS_TRACE
+    // debug: boundary timestamps of CTA 0 (epilogue thread m = 0, MMA issuer), printed at exit
+    long long tr[12][8];
+    for (int a = 0; a < 12; ++a) for (int b = 0; b < 8; ++b) tr[a][b] = 0;
+    const bool trc = blockIdx.x == 0 && ((warp == 2 && lane == 0) || (warp == 1 && lane == 0));
+#define TRACE(slot) do { if (trc && round < 12) tr[round][slot] = clock64(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
     for (;;) {
+        TRACE(4);
         const int loc = __syncthreads_or(epi && active);
+        TRACE(5);
         if (tid == 0) {
             const uint32_t off = 4u * (2u * (round & 1u) + rank);
             st_cluster_u32(flags_self + off, (uint32_t)loc);
@@ -215,7 +246,9 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             dirty = 0u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
+        TRACE(6);
         cluster_sync();   // both A tiles ready; both flags visible
+        TRACE(7);
         const uint32_t any = flags[2 * (round & 1u)] | flags[2 * (round & 1u) + 1];
         ++round;
         if (!any) break;
@@ -236,6 +269,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                     const uint32_t buf = pc_m & 1u;
                     mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
                     tc_fence_after();
+                    if (pass == 0) TRACE(0);
                     const uint32_t idesc = i8_idesc_pair(ncols);
                     for (int kb = 0; kb < nkb; ++kb, ++it_m) {
                         const int st = it_m % S;
@@ -256,11 +290,13 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             // ---- epilogue: per-cluster max + mask of each pass (a4)
             const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
             fetch_syms();
+            flush();
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
                 const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
                 const uint32_t buf = pc_e & 1u;
                 mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
                 tc_fence_after();
+                if (pass == npass - 1) TRACE(1);
                 for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
                     const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
                     if constexpr (WC <= 4) {
@@ -327,23 +363,31 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                 tc_fence_before();
                 mbar_arrive_cluster(tempty_leader0 + 8u * buf);
             }
+            TRACE(2);
             if (active) {   // convergence (Alg. 1 "until V^{t+1} == V^t") and slot refill
                 ++rl;
                 const bool cyc_stop = P.cyc && rl >= 2 && cyc && changed;   // V^r == V^{r-2}
-                if (!changed || rl == T || cyc_stop) {   // ---- a7 output
-                    uint32_t *out = out_state + p * nw;
-                    for (int w = 0; w < nw; ++w) out[w] = Vn[w * kTM + m];
+                if (!changed || rl == T || cyc_stop) {   // ---- a7 output (state: flush)
+                    pend = p;
                     out_iters[p] = (uint16_t)rl;
                     out_status[p] = (uint8_t)(!changed ? GB_CONVERGED : cyc_stop ? GB_CYCLE : GB_MAX_ITERS);
                     dirty |= nzcur;
-                    refill();
+                    refill(nzcur);
                 } else {
                     par ^= 1u;
                 }
             }
             nzcur = 0u;
+            TRACE(3);
         }
     }
+    if (epi) flush();
+#ifdef GB_SOS_TRACE
+    if (trc)
+        for (int a = 0; a < 12; ++a)
+            printf("TRACE w%d r%d mma0 %lld lastdone %lld epidone %lld refilled %lld top %lld syncor %lld aupd %lld csync %lld\n",
+                   warp, a, tr[a][0], tr[a][1], tr[a][2], tr[a][3], tr[a][4], tr[a][5], tr[a][6], tr[a][7]);
+#endif
     // drain the prefetched loads (both halves complete on the leader's full barriers)
     // before either CTA can exit
     if (warp == 0 && lane == 0 && leader)

@@ -33,7 +33,7 @@ KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio")
 # capture -> (summary name, traffic key)
 CAPS = {"prof_hyb": ("hyb", "c3"), "prof_sos": ("sos", "c2"), "prof_sosc4": ("sos_c4", "c4"),
-        "prof_l2": ("l2", "c4"), "prof_store": ("store", "c5")}
+        "prof_l2": ("l2", "c4"), "prof_store": ("store", "c5"), "prof_smem": ("smem", "c2som")}
 
 
 def raw(rep):
@@ -48,7 +48,7 @@ def to_bytes(u, v):
 
 
 # probes per launch of the captures whose shared-memory wavefronts are reported per probe
-PROBES = {"prof_hyb": 10_000_000}   # kernels whose W rows live in shared memory
+PROBES = {"prof_hyb": 10_000_000, "prof_smem": 1_000_000}   # kernels whose W rows live in shared memory
 traffic = {}
 for cap, (name, cfg) in CAPS.items():
     rep = os.path.join(G, f"{cap}_{TAG}.ncu-rep")
@@ -76,10 +76,11 @@ for src, dst in ((f"bench_full_{TAG}.json", f"{RND}_bench_c3.json"),
                  (f"bench_ref_{TAG}.json", f"{RND}_bench_reference_c3.json"),
                  (f"bench_rules_{TAG}.jsonl", f"{RND}_bench_rules.jsonl"),
                  (f"launches_{TAG}.csv", f"{RND}_launches_c3.csv"),
-                 (f"tests_{TAG}.txt", f"{RND}_tests.txt"), (f"smoke_{TAG}.txt", f"{RND}_smoke.txt")):
+                 (f"tests_{TAG}.txt", f"{RND}_tests.txt"), (f"smoke_{TAG}.txt", f"{RND}_smoke.txt"),
+                 (f"motivation_{TAG}.json", f"{RND}_motivation.json")):
     s = os.path.join(G, src)
     if os.path.exists(s):
-        if dst.endswith(".json"):   # the JSON line only
+        if dst.endswith(".json") and "motivation" not in dst:   # the JSON line only
             lines = [l for l in open(s) if l.startswith("{")]
             open(os.path.join(P, dst), "w").write(lines[-1] if lines else "")
         else:
