@@ -1,6 +1,7 @@
 // gb_decode_sos_tc3.cu -- sum-of-sum decode on the tensor cores for networks
 // whose expanded A tile does not fit in shared memory (1024 < n_p <= 4096,
-// Lp <= 256; BASELINE C4: c=16 l=256, n_p = 4096).
+// Lp <= 256; BASELINE C4: c=16 l=256, n_p = 4096; on the CTA pair also Lp = 512
+// up to n_p = 8192, the paper's Scenario 2: c=16 l=512).
 //
 // Same method and per-probe semantics as sos_tc2_kernel (gb_decode_sos_tc.cu):
 // a3 S^t = W V^t + gamma V^t as an exact int8 x int8 -> int32 contraction
@@ -48,6 +49,7 @@ struct Sos3Params {
     int SA;          // A stages
     int gamma_epi;   // gamma added in the epilogue (0 when folded into B)
     int cyc;         // GB_FLAG_CYCLE_EXIT: stop a probe when V^r == V^{r-2}
+    int vglob;       // current state in the global scratch (n_p > 4096: too big for shared memory)
     uint32_t a_off, b_off, v_off, bar_off, b_stage;
 };
 
@@ -295,7 +297,7 @@ cudaError_t launch3_t(Call &cl, const Sos3Params &P, size_t smem, const CUtensor
 // (leader's, 256 arrivals: both epilogues); empty / aempty / tfull receive the
 // pair's multicast commits in both CTAs.  Rounds are cluster-wide (flags + cluster
 // barrier), as in sos_tc2x2_kernel.
-template <int WC>
+template <int WC, bool VG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads3, 1)
 sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P,
                  const uint16_t *__restrict__ probes, int64_t k, int T, unsigned long long *queue,
@@ -308,7 +310,6 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
     uint8_t *gbase = smem_raw + (base - raw);
     const uint32_t A0 = base + P.a_off;     // SA x (128 x 128 B): this CTA's probe rows
     const uint32_t B0 = base + P.b_off;     // S x (NP/2 x 128 B): this CTA's half of the W rows
-    uint32_t *V = reinterpret_cast<uint32_t *>(gbase + P.v_off);
     uint64_t *bars = reinterpret_cast<uint64_t *>(gbase + P.bar_off);
     const uint32_t bar0 = smem_u32(bars);
     const int S = P.S, SA = P.SA;
@@ -331,7 +332,17 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
     const int nw = s.nw, np = s.np;
     const int nkb = (np + kKB - 1) / kKB;
     const int npass = (np + P.NP - 1) / P.NP;
-    uint32_t *Vn2 = vscratch + (size_t)blockIdx.x * 2 * nw * kTM;
+    // global scratch per CTA: two next-state areas (as in sos_tc3_kernel) and, when it does not
+    // fit shared memory (n_p > 4096), the current state
+    uint32_t *Vn2 = vscratch + (size_t)blockIdx.x * 3 * nw * kTM;
+    uint32_t *V = VG ? Vn2 + 2 * nw * kTM : reinterpret_cast<uint32_t *>(gbase + P.v_off);   // compile-time space
+    // TMEM: two 256-column accumulators (the epilogue of pass p overlaps pass p+1), or one of 512
+    // columns when a cluster is wider than 256 (Lp = 512: one cluster per pass, MMAs of N = 256
+    // into its two halves; the epilogue then runs between passes).  Scenario 2 (c=16 l=512, 3*10^4
+    // probes) 8.28 ms on the 4-warp sos_tc_kernel -> 4.46 ms here (same-box A/B).  Both counts are
+    // compile-time: with runtime sub-tile loops in the MMA issuer C4 ran 28 ms instead of 18.
+    constexpr int NB = WC > 8 ? 1 : 2;   // WC = 16 <=> Lp = 512 (plan3)
+    constexpr int NSUB = WC > 8 ? 2 : 1;
 
     if (tid == 0) {
         for (int i = 0; i < S; ++i) { mbar_init(full_bar(i), 1); mbar_init(empty_bar(i), 1); }
@@ -402,15 +413,19 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
         if (warp == 0) {
             if (lane == 0) {   // ---- TMA: this CTA's half of each pass's W rows, K block by K block
                 for (int pass = 0; pass < npass; ++pass) {
-                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0), half = ncols >> 1;
+                    // sub-tiles of <= 256 columns (one MMA each); this CTA stages half of each
+                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    const int nsc = ncols / NSUB, half = nsc >> 1;
                     for (int kb = 0; kb < nkb; ++kb, ++it_p) {
                         const int st = it_p % S;
                         mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
                         if (leader) mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);   // both halves
                         const uint32_t Bs = B0 + st * P.b_stage;
-                        for (int r0 = 0; r0 < half; r0 += P.BR)
-                            tma_load_2d_pair(Bs + r0 * kKB, &wmap, full_leader0 + 8u * st, kb * kKB,
-                                             n0 + (int)rank * half + r0);
+#pragma unroll
+                        for (int j = 0; j < NSUB; ++j)
+                            for (int r0 = 0; r0 < half; r0 += P.BR)
+                                tma_load_2d_pair(Bs + (j * half + r0) * kKB, &wmap, full_leader0 + 8u * st, kb * kKB,
+                                                 n0 + j * nsc + (int)rank * half + r0);
                     }
                 }
             }
@@ -419,10 +434,11 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
             if (lane == 0 && leader) {   // ---- MMA issuer for the pair
                 for (int pass = 0; pass < npass; ++pass, ++pc_m) {
                     const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
-                    const uint32_t buf = pc_m & 1u;
-                    mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
+                    const int nsc = ncols / NSUB, half = nsc >> 1;
+                    const uint32_t buf = pc_m % NB, use = pc_m / NB;
+                    mbar_wait(tempty_bar(buf), (use & 1u) ^ 1u);
                     tc_fence_after();
-                    const uint32_t idesc = i8_idesc_pair(ncols);
+                    const uint32_t idesc = i8_idesc_pair(nsc);
                     for (int kb = 0; kb < nkb; ++kb, ++it_m) {
                         const int st = it_m % S, sa = it_m % SA;
                         mbar_wait(afull_bar(sa), (it_m / SA) & 1u);
@@ -431,8 +447,11 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
                         const uint32_t As = A0 + sa * (kTM * kKB), Bs = B0 + st * P.b_stage;
 #pragma unroll
                         for (int ks = 0; ks < kKB / 32; ++ks)
-                            umma_i8_pair(tmem + buf * 256, sw128_desc(As + ks * 32), sw128_desc(Bs + ks * 32), idesc,
-                                         (kb > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+                            for (int j = 0; j < NSUB; ++j)
+                                umma_i8_pair(tmem + buf * 256 + j * 256, sw128_desc(As + ks * 32),
+                                             sw128_desc(Bs + j * half * kKB + ks * 32), idesc,
+                                             (kb > 0 || ks > 0) ? 1u : 0u);
                         umma_commit_pair(empty_bar(st));
                         umma_commit_pair(aempty_bar(sa));
                     }
@@ -471,35 +490,52 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
             bool changed = false, cyc = true;
             uint32_t *Vn = Vn2 + (size_t)((rl + 1) & 1) * nw * kTM;
             const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+#ifndef GB_TC3_GB
+#define GB_TC3_GB 2
+#endif
+            constexpr int GB = WC < GB_TC3_GB ? WC : GB_TC3_GB;   // TMEM loads in flight per wait
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
                 const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
-                const uint32_t buf = pc_e & 1u;
-                mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
+                const uint32_t buf = pc_e % NB;
+                mbar_wait(tfull_bar(buf), (pc_e / NB) & 1u);
                 tc_fence_after();
                 for (int c = n0 / LP; c < (n0 + ncols) / LP; ++c) {
                     const uint32_t col = buf * 256 + (uint32_t)(c * LP - n0);
                     uint32_t mx = 0;
-                    for (int g = 0; g < WC; ++g) {
-                        uint32_t v32[32];
-                        tmem_ld32(tl + col + 32 * g, v32);
-                        const uint32_t vw = P.gamma_epi ? V[(c * WC + g) * kTM + m] : 0u;
+                    for (int g0 = 0; g0 < WC; g0 += GB) {
+                        uint32_t v[GB][32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            mx = max(mx, v32[j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                        for (int gg = 0; gg < GB; ++gg) tmem_ld32_nw(tl + col + 32 * (g0 + gg), v[gg]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int gg = 0; gg < GB; ++gg) {
+                            tmem_regs_ready(v[gg]);
+                            const uint32_t vw = P.gamma_epi ? V[(c * WC + g0 + gg) * kTM + m] : 0u;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                mx = max(mx, v[gg][j] + (((vw >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u));
+                        }
                     }
-                    for (int g = 0; g < WC; ++g) {
-                        uint32_t v32[32];
-                        tmem_ld32(tl + col + 32 * g, v32);
-                        const uint32_t vw = V[(c * WC + g) * kTM + m];
-                        const uint32_t ve = P.gamma_epi ? vw : 0u;
-                        uint32_t word = 0;
+                    for (int g0 = 0; g0 < WC; g0 += GB) {
+                        uint32_t v[GB][32];
 #pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            word |= ((v32[j] + (((ve >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
-                        word &= real_mask(s.L, g);
-                        if (word != vw) changed = true;
-                        if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
-                        Vn[(c * WC + g) * kTM + m] = word;
+                        for (int gg = 0; gg < GB; ++gg) tmem_ld32_nw(tl + col + 32 * (g0 + gg), v[gg]);
+                        tmem_wait_ld();
+#pragma unroll
+                        for (int gg = 0; gg < GB; ++gg) {
+                            tmem_regs_ready(v[gg]);
+                            const int g = g0 + gg;
+                            const uint32_t vw = V[(c * WC + g) * kTM + m];
+                            const uint32_t ve = P.gamma_epi ? vw : 0u;
+                            uint32_t word = 0;
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                word |= ((v[gg][j] + (((ve >> j) & 1u) ? (uint32_t)P.gamma_epi : 0u)) == mx ? 1u : 0u) << j;
+                            word &= real_mask(s.L, g);
+                            if (word != vw) changed = true;
+                            if (P.cyc) cyc &= (Vn[(c * WC + g) * kTM + m] == word);   // V^{r-2}
+                            Vn[(c * WC + g) * kTM + m] = word;
+                        }
                     }
                 }
                 tc_fence_before();
@@ -531,11 +567,12 @@ cudaError_t launch3x2_t(Call &cl, const Sos3Params &P, size_t smem, const CUtens
                         uint8_t *status) {
     const gb_net *net = cl.net;
     const cudaStream_t st = cl.st;
-    auto fn = sos_tc3x2_kernel<WC>;
+    auto fn = P.vglob ? sos_tc3x2_kernel<WC, true> : sos_tc3x2_kernel<WC, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    static std::atomic<int> max_clusters[9];
-    if (max_clusters[WC].load() == 0) {
+    static std::atomic<int> max_clusters[17][2];
+    std::atomic<int> &mc = max_clusters[WC][P.vglob ? 1 : 0];
+    if (mc.load() == 0) {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -552,11 +589,11 @@ cudaError_t launch3x2_t(Call &cl, const Sos3Params &P, size_t smem, const CUtens
             cudaGetLastError();
             n = net->sm_count / 2;
         }
-        max_clusters[WC].store(n);
+        mc.store(n);
     }
     const int64_t npairs = (k + 2 * kTM - 1) / (2 * kTM);
-    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC].load()));
-    uint32_t *vscratch = cl.alloc_n<uint32_t>((size_t)2 * pairs * 2 * net->s.nw * kTM);
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, mc.load()));
+    uint32_t *vscratch = cl.alloc_n<uint32_t>((size_t)2 * pairs * 3 * net->s.nw * kTM);
     unsigned long long *queue = cl.counters();
     if (!vscratch || !queue) return cl.err;
     fn<<<2 * pairs, kThreads3, smem, st>>>(net->s, *map, P, probes, k, max_iters, queue, vscratch, state,
@@ -574,21 +611,26 @@ static bool pair3_enabled(const gb_net *net) {
 bool plan3(const gb_net *net, int gamma, void *params, size_t &smem) {
     const Shape &s = net->s;
     Sos3Params &P = *reinterpret_cast<Sos3Params *>(params);
-    if (s.Lp > 256 || s.np <= 1024 || s.np > 4096) return false;
-    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4 && s.Wc != 8) return false;
-    P.NP = s.Lp * (256 / s.Lp);
-    if (P.NP > s.np) P.NP = s.np;
     const bool pair = pair3_enabled(net);
-    // pair: each CTA stages half of every pass (whole clusters -> halves of Lp/2 rows)
+    // 1024 < n_p <= 4096 with Lp <= 256 (both forms); Scenario 2's Lp = 512 up to n_p = 8192 on the
+    // CTA pair only (one 512-column accumulator, current state in the global scratch)
+    if (s.np <= 1024 || s.np > (pair ? 8192 : 4096)) return false;
+    if (s.Wc != 1 && s.Wc != 2 && s.Wc != 4 && s.Wc != 8 && !(pair && s.Wc == 16)) return false;
+    P.NP = s.Lp > 256 ? s.Lp : s.Lp * (256 / s.Lp);
+    if (P.NP > s.np) P.NP = s.np;
+    // pair: each CTA stages half of every <= 256-column sub-tile (whole clusters -> halves of
+    // Lp/2 rows, or 128 rows of a 512-column pass)
     const int rows = pair ? P.NP / 2 : P.NP;
+    const int unit = pair ? (P.NP > 256 ? 128 : s.Lp / 2) : s.Lp;
     int br = 256;
-    while (br > 8 && ((pair ? s.Lp / 2 : s.Lp) % br || br > rows)) br >>= 1;
+    while (br > 8 && (unit % br || br > rows)) br >>= 1;
     P.BR = br;
     P.gamma_epi = gamma > 255 ? gamma : 0;
     P.cyc = 0;
+    P.vglob = s.np > 4096 ? 1 : 0;
     P.b_stage = (uint32_t)rows * kKB;
     P.b_stage = (P.b_stage + 1023u) & ~1023u;   // SW128 atoms stay 1024-byte aligned
-    const size_t vbytes = (size_t)s.nw * kTM * 4;
+    const size_t vbytes = P.vglob ? 0 : (size_t)s.nw * kTM * 4;
     int s_max = pair ? 6 : 4, sa_max = 3;
     for (P.S = s_max; P.S >= 2; --P.S) {
         for (P.SA = sa_max; P.SA >= 2; --P.SA) {
@@ -629,7 +671,8 @@ cudaError_t launch_sos_tc3(Call &cl, int gamma, int cyc, const void *map, const 
             case 1: return launch3x2_t<1>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
             case 2: return launch3x2_t<2>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
             case 4: return launch3x2_t<4>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
-            default: return launch3x2_t<8>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+            case 8: return launch3x2_t<8>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
+            default: return launch3x2_t<16>(cl, P, smem, m, probes, k, max_iters, state, iters, status);
         }
     }
     switch (net->s.Wc) {

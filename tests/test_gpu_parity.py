@@ -439,7 +439,7 @@ def test_determinism(gb):
                                            (4, 16, 2, "decode_smem_kernel"),
                                            (16, 256, 1, "decode_l2t_kernel"), (16, 256, 2, "decode_l2t_kernel"),
                                            (12, 40, 2, "decode_l2_kernel"), (9, 100, 1, "decode_l2t_kernel"),
-                                           (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc_kernel"),
+                                           (9, 70, 1, "decode_generic_kernel"), (16, 512, 0, "sos_tc3x2_kernel"),
                                            (16, 512, 2, "decode_l2t_kernel"), (16, 512, 1, "decode_l2t_kernel"),
                                            (4, 600, 0, "decode_generic_kernel")])
 def test_kernel_selection(gb, c, l, rule, want):
@@ -452,6 +452,9 @@ def test_kernel_selection(gb, c, l, rule, want):
         assert net.decode_kernel(rule) == want.replace("_kernel", "x2_kernel")
         net.set_option("sos_pair", 0)
     assert net.decode_kernel(rule) == want
+    if want == "sos_tc3x2_kernel":   # Lp = 512 / n_p > 4096: streamed A on the CTA pair only
+        net.set_option("sos_pair", 0)
+        assert net.decode_kernel(0) == "sos_tc_kernel"
 
 
 @pytest.mark.parametrize("rule", RULES)
@@ -610,6 +613,33 @@ def test_sos_streamed_a_vs_oracle(gb, c, l, m, e, gamma, k):
     net.close()
 
 
+@pytest.mark.parametrize("c,l,m,e,gamma,k", [(16, 512, 50000, 7, 2, 600), (10, 500, 20000, 5, 0, 300),
+                                             (3, 512, 200, 1, 300, 129), (16, 512, 5000, 12, 255, 257)])
+def test_sos_streamed_a_wide_clusters(gb, c, l, m, e, gamma, k):
+    """Scenario 2's shape (Lp = 512, n_p up to 8192) on the streamed-A CTA-pair kernel: one
+    512-column accumulator per pass (two N = 256 MMAs), the current state in the global
+    scratch.  Bit-exact vs the oracle and the 4-warp sos_tc_kernel (GB_OPT_SOS_PAIR = 0):
+    ragged L (500), gamma 0 / folded (2, 255) / in the epilogue (300), T = 3, invalid and
+    random probes."""
+    msgs = gbgen.messages(900 + c + l, m, c, l)
+    net = make_net(gb, msgs, c, l)
+    pr, _ = gbgen.probes(901 + c, msgs, k, e, l, random_count=k // 10)
+    pr[2, 0] = l                       # invalid symbol
+    w8, _ = oracle.store(msgs, c, l)
+    if c * 512 > 1024:
+        assert net.decode_kernel(0) == "sos_tc3x2_kernel"
+    want = oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=20)
+    got = gpu_decode(net, pr, 0, gamma, 20)
+    assert_same(got, want, 0, "wide pair")
+    assert_same(gpu_decode(net, pr, 0, gamma, 3), oracle.decode(w8, c, l, pr, oracle.SOS, gamma=gamma, max_iters=3),
+                0, "wide pair T=3")
+    net.set_option("sos_pair", 0)
+    other = gpu_decode(net, pr, 0, gamma, 20)
+    for x, y in zip(got, other):
+        np.testing.assert_array_equal(x, y)
+    net.close()
+
+
 @pytest.mark.parametrize("c,l,m,e,k", [(16, 256, 100000, 8, 300), (16, 256, 20000, 11, 200), (12, 100, 3000, 5, 257),
                                        (16, 512, 50000, 7, 100), (9, 128, 8000, 3, 129), (16, 200, 0, 6, 64)])
 @pytest.mark.parametrize("rule", [1, 2])
@@ -648,7 +678,8 @@ def test_l2t_matches_oracle_and_warp_kernel(gb, c, l, m, e, k, rule):
     (16, 256, 100000, 10, 300, 0, {}, "sos_tc3x2_kernel"),
     (16, 256, 100000, 10, 300, 0, {"sos_pair": 0}, "sos_tc3_kernel"),
     (16, 256, 100000, 10, 300, 0, {"sos_streamed": 0}, "sos_tc_kernel"),
-    (8, 512, 30000, 5, 200, 0, {}, "sos_tc_kernel"),
+    (8, 512, 30000, 5, 200, 0, {}, "sos_tc3x2_kernel"),
+    (8, 512, 30000, 5, 200, 0, {"sos_pair": 0}, "sos_tc_kernel"),
     (4, 600, 3000, 2, 100, 0, {}, "decode_generic_kernel"),
 ])
 def test_sos_cycle_exit_flag(gb, c, l, m, e, k, gamma, opts, kernel):
