@@ -480,18 +480,38 @@ def test_config2_full_size_sampled(gb, rule):
 
 
 def test_config4_full_size_sampled(gb):
-    """BASELINE config 4 (c=16 l=256, M=10^5, e=8) at 10^5 probes for SOS and SOM
-    (the bench's side measurement), 12 sampled probes per rule vs the oracle."""
-    c, l, m, k = 16, 256, 100_000, 100_000
+    """BASELINE config 4 (c=16 l=256, M=10^5, e=8) at the bench's size (K=10^6, the launch
+    configuration bench.py times: sos_tc3x2_kernel / decode_l2t_kernel) for SOS and SOM:
+    48 sampled probes per rule vs the oracle (the batch's first and last probes among them),
+    and over all K the properties that hold at any size -- no invalid status, rounds in
+    [1, 20]; SOS: every cluster keeps at least one neuron (the max is always attained,
+    Eq.(5)); SOM: every stored source message is contained in its final state (Lemma 3)."""
+    c, l, m, k = 16, 256, 100_000, 1_000_000
     msgs = gbgen.messages(0x5EED, m, c, l)
-    pr, _ = gbgen.probes(0x5EED + 1, msgs, k, 8, l)
+    pr, src = gbgen.probes(0x5EED + 1, msgs, k, 8, l)
     net = make_net(gb, msgs, c, l)
     w, _ = oracle.store(msgs, c, l)
-    idx = np.array([0, 1, 2, 777, 12345, 33333, 50000, 65432, 80000, 99997, 99998, 99999])
+    rng = np.random.default_rng(44)
+    idx = np.unique(np.concatenate([[0, 1, k - 2, k - 1], rng.choice(k, 44, replace=False)]))
+    wc = 8
+    msg_d = torch.from_numpy(msgs[src].astype(np.int64)).cuda()
+    cols = torch.arange(c, device="cuda") * wc + (msg_d >> 5)
+    bit = torch.bitwise_left_shift(torch.ones_like(msg_d), msg_d & 31)
     for rule in (0, 1):
-        st, it, ss = gpu_decode(net, pr, rule, 2, 20)
-        assert_same((st[idx], it[idx], ss[idx]), oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule,
-                    "config4 sampled")
+        assert net.decode_kernel(rule) == ("sos_tc3x2_kernel" if rule == 0 else "decode_l2t_kernel")
+        st, it, ss = net.decode(to_dev(pr), rule, gamma=2, max_iters=20)
+        torch.cuda.synchronize()
+        assert int((ss == 2).sum()) == 0
+        its = it.to(torch.int32) & 0xFFFF
+        assert int(its.min()) >= 1 and int(its.max()) <= 20
+        if rule == 0:
+            blocks = (st.view(k, c, wc).to(torch.int64) & 0xFFFFFFFF).ne(0).any(dim=2)
+            assert bool(blocks.all())
+        else:
+            words = torch.gather(st, 1, cols).to(torch.int64) & 0xFFFFFFFF
+            assert bool((words & bit).ne(0).all())
+        got = (st[idx].cpu().numpy().view(np.uint32), it[idx].cpu().numpy().view(np.uint16), ss[idx].cpu().numpy())
+        assert_same(got, oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule, "config4 sampled")
 
 
 def test_config4_hybrid_full_size_sampled(gb):
