@@ -30,9 +30,31 @@ namespace {
 
 constexpr int kMaxC16 = 16;
 
+#ifndef GB_L2T_V8
+#define GB_L2T_V8 1
+#endif
+// 32-byte read-only load (sm_100: LDG.256): one sector per lane, half the L1TEX wavefronts of two
+// 16-byte loads of the same block (the kernel is bound by the L1TEX data pipe: 93% at C4 with
+// 16-byte loads).  Same-box A/B: C4 hybrid 2.05 -> 1.59 ms, C4 sum-of-max (10^6) 10.56 -> 9.13,
+// Scenario 2 sum-of-max 1.745 -> 1.689, hybrid 0.174 -> 0.167.
+__device__ __forceinline__ void ldg8(const uint32_t *a, uint32_t *v) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(a));
+}
+__device__ __forceinline__ void ldg8p(uint32_t p, const uint32_t *a, uint32_t *v) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %8, 0;\n\t@q ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%9];\n\t}"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5]), "+r"(v[6]), "+r"(v[7])
+        : "r"(p), "l"(a));
+}
+
 template <int WC>
 __device__ __forceinline__ void ldg_block(const uint32_t *p, uint32_t (&v)[WC]) {
-    if constexpr (WC % 4 == 0) {
+    if constexpr (GB_L2T_V8 && WC % 8 == 0) {
+#pragma unroll
+        for (int q = 0; q < WC / 8; ++q) ldg8(p + 8 * q, v + 8 * q);
+    } else if constexpr (WC % 4 == 0) {
 #pragma unroll
         for (int q = 0; q < WC / 4; ++q) {
             const uint4 t = __ldg(reinterpret_cast<const uint4 *>(p) + q);
@@ -56,11 +78,21 @@ __device__ __forceinline__ void ldg4p(uint32_t p, const uint32_t *a, uint32_t (&
 template <int WC>
 __device__ __forceinline__ void ldg_blockp(uint32_t p, const uint32_t *a, uint32_t (&v)[WC]) {
     static_assert(WC % 4 == 0, "predicated block loads need Wc % 4 == 0");
+    if constexpr (GB_L2T_V8 && WC % 8 == 0) {
 #pragma unroll
-    for (int q = 0; q < WC / 4; ++q) {
-        uint32_t t[4] = {0u, 0u, 0u, 0u};
-        ldg4p(p, a + 4 * q, t);
-        v[4 * q] = t[0]; v[4 * q + 1] = t[1]; v[4 * q + 2] = t[2]; v[4 * q + 3] = t[3];
+        for (int q = 0; q < WC / 8; ++q) {
+            uint32_t t[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+            ldg8p(p, a + 8 * q, t);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[8 * q + i] = t[i];
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < WC / 4; ++q) {
+            uint32_t t[4] = {0u, 0u, 0u, 0u};
+            ldg4p(p, a + 4 * q, t);
+            v[4 * q] = t[0]; v[4 * q + 1] = t[1]; v[4 * q + 2] = t[2]; v[4 * q + 3] = t[3];
+        }
     }
 }
 
