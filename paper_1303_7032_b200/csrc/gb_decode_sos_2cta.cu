@@ -31,6 +31,13 @@
 #include "gb_internal.h"
 #include "gb_tc_common.cuh"
 
+#ifndef GB_SOS_STATIC
+#define GB_SOS_STATIC 1
+#endif
+#ifndef GB_SOS_AUPD2
+#define GB_SOS_AUPD2 4
+#endif
+
 namespace gb {
 namespace {
 using namespace tc;
@@ -138,7 +145,15 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             const uint4 q = qn;
             fetch();
             uint32_t *Vc = Vs + par * nw * kTM;
+#if GB_SOS_STATIC
+            // static predicated loop over the <= 32 state words (n_p <= 1024): no divergent
+            // loop, stores independent
+#pragma unroll
+            for (int w = 0; w < 32; ++w)
+                if ((zmask >> w) & 1u) Vc[w * kTM + m] = 0u;
+#else
             for (uint32_t d = zmask; d; d &= d - 1u) Vc[(__ffs(d) - 1) * kTM + m] = 0u;
+#endif
             zmask = 0u;
             rl = 0;
             if (p >= k) { active = false; return; }
@@ -150,9 +165,17 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                 return __ldg(probes + p * s.C + c);
             };
             bool valid = true;
-            for (int c = 0; c < s.C; ++c) {
-                const unsigned sym = sym_of(c);
-                if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+            if (pack) {   // C <= 8: symbols in registers, static unroll
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const unsigned sym = sym_of(c);
+                    if (c < s.C && sym != kErased && sym >= (unsigned)s.L) valid = false;
+                }
+            } else {
+                for (int c = 0; c < s.C; ++c) {
+                    const unsigned sym = sym_of(c);
+                    if (sym != kErased && sym >= (unsigned)s.L) valid = false;
+                }
             }
             if (!valid) {   // GB_INVALID: zero state, 0 rounds; take another probe
                 uint32_t *out = out_state + p * nw;
@@ -161,13 +184,20 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                 out_status[p] = GB_INVALID;
                 continue;
             }
-            for (int c = 0; c < s.C; ++c) {   // a1 ingest: V^0 known one-hot
+            auto ingest = [&](int c) {   // a1 ingest: V^0 known one-hot
                 const unsigned sym = sym_of(c);
                 if (sym != kErased) {
                     const int w = c * WC + (int)(sym >> 5);
                     Vc[w * kTM + m] = 1u << (sym & 31);
                     dirty |= 1u << w;
                 }
+            };
+            if (pack) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c)
+                    if (c < s.C) ingest(c);
+            } else {
+                for (int c = 0; c < s.C; ++c) ingest(c);
             }
             active = true;
             return;
@@ -193,8 +223,11 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     // set.  Round boundary at C2 (clock64 trace of CTA 0, GB_SOS_TRACE builds): last pass's
     // epilogue 1.7k cycles, convergence + output + refill 3.4k -> 2.4k, A update 2.2k, cluster
     // barrier 0.6-3k, against 21.5k cycles of MMAs per round; C2 10^6 probes 2.72 -> 2.59 ms.
+    // Then the refill's zeroing as a static predicated loop (2.4k -> 1.6k cycles) and the A update
+    // four dirty words per iteration (2.2k -> ~1.7k): 2.60 -> 2.47-2.51 ms (same-box A/Bs).
     // Measured and not kept: the A update K block by K block with the next block's state words
-    // loaded ahead (5.4k cycles, 2.81 ms).
+    // loaded ahead (5.4k cycles, 2.81 ms), and as a static predicated loop over all 32 words
+    // (4.3k cycles).
     int64_t pend = -1;
     auto flush = [&]() {
         if (pend >= 0) {
@@ -228,6 +261,37 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         bool changed = false;
         bool cyc = true;
         if (epi) {   // incremental A = V^T (bytes, SW128), as in sos_tc2_kernel
+#if GB_SOS_AUPD2
+            // GB_SOS_AUPD2 dirty words per iteration: their state-word loads and expansions
+            // overlap (one word at a time, each store waited on its load: 2.2k cycles per round
+            // boundary at C2; two at a time 1.8k)
+            constexpr int NA = GB_SOS_AUPD2;
+            uint32_t d = dirty;
+            while (d) {
+                int wq[NA];
+                uint32_t vq[NA];
+#pragma unroll
+                for (int q = 0; q < NA; ++q) {
+                    wq[q] = d ? __ffs(d) - 1 : -1;
+                    d &= d - 1u;
+                    vq[q] = (wq[q] >= 0 && wq[q] < nw) ? V[wq[q] * kTM + m] : 0u;
+                }
+#pragma unroll
+                for (int q = 0; q < NA; ++q) {
+                    if (wq[q] < 0) continue;
+                    const int w = wq[q];
+                    uint8_t *arow = gbase + P.a_off + (w >> 2) * (kTM * kKB) + m * kKB;
+#pragma unroll
+                    for (int h2 = 0; h2 < 2; ++h2) {
+                        const int ch = 2 * (w & 3) + h2;
+                        const uint32_t bits = (vq[q] >> (h2 * 16)) & 0xffffu;
+                        *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
+                            make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
+                                       spread4((bits >> 8) & 15u), spread4(bits >> 12));
+                    }
+                }
+            }
+#else
             uint32_t d = dirty;
             while (d) {
                 const int w = __ffs(d) - 1;
@@ -243,6 +307,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                                    spread4((bits >> 8) & 15u), spread4(bits >> 12));
                 }
             }
+#endif
             dirty = 0u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
