@@ -2,7 +2,8 @@
 
 Covers every kernel family: store (scattered + privatised) + apply + seal, OR of packed
 partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l2 (list mode),
-SOS pair / streamed-A / 4-warp / generic, the cycle-exit flag, and the tensor-core SOM kernel.
+SOS pair / streamed-A (incl. Lp = 512 with the state in the global scratch) / 4-warp / generic,
+the cycle-exit flag, and the tensor-core SOM kernel.
 """
 import sys
 import numpy as np
@@ -13,7 +14,7 @@ import paper_1303_7032_b200 as gb
 
 for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 500, 100, 5), (3, 3, 4, 20, 2),
                         (16, 256, 20000, 150, 8), (12, 100, 3000, 100, 5), (8, 512, 3000, 64, 4),
-                        (4, 600, 300, 50, 2)):
+                        (16, 512, 3000, 40, 7), (4, 600, 300, 50, 2)):
     msgs = gbgen.messages(1, m, c, l)
     pr, _ = gbgen.probes(2, msgs, k, e, l, random_count=k // 10)
     rng = np.random.default_rng(k)
