@@ -30,9 +30,6 @@ namespace {
 
 constexpr int kMaxC16 = 16;
 
-#ifndef GB_L2T_V8
-#define GB_L2T_V8 1
-#endif
 // 32-byte read-only load (sm_100: LDG.256): one sector per lane, half the L1TEX wavefronts of two
 // 16-byte loads of the same block (the kernel is bound by the L1TEX data pipe: 93% at C4 with
 // 16-byte loads).  Same-box A/B: C4 hybrid 2.05 -> 1.59 ms, C4 sum-of-max (10^6) 10.56 -> 9.13,
@@ -51,7 +48,7 @@ __device__ __forceinline__ void ldg8p(uint32_t p, const uint32_t *a, uint32_t *v
 
 template <int WC>
 __device__ __forceinline__ void ldg_block(const uint32_t *p, uint32_t (&v)[WC]) {
-    if constexpr (GB_L2T_V8 && WC % 8 == 0) {
+    if constexpr (WC % 8 == 0) {
 #pragma unroll
         for (int q = 0; q < WC / 8; ++q) ldg8(p + 8 * q, v + 8 * q);
     } else if constexpr (WC % 4 == 0) {
@@ -78,7 +75,7 @@ __device__ __forceinline__ void ldg4p(uint32_t p, const uint32_t *a, uint32_t (&
 template <int WC>
 __device__ __forceinline__ void ldg_blockp(uint32_t p, const uint32_t *a, uint32_t (&v)[WC]) {
     static_assert(WC % 4 == 0, "predicated block loads need Wc % 4 == 0");
-    if constexpr (GB_L2T_V8 && WC % 8 == 0) {
+    if constexpr (WC % 8 == 0) {
 #pragma unroll
         for (int q = 0; q < WC / 8; ++q) {
             uint32_t t[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};

@@ -31,12 +31,6 @@
 #include "gb_internal.h"
 #include "gb_tc_common.cuh"
 
-#ifndef GB_SOS_STATIC
-#define GB_SOS_STATIC 1
-#endif
-#ifndef GB_SOS_AUPD2
-#define GB_SOS_AUPD2 4
-#endif
 
 namespace gb {
 namespace {
@@ -145,15 +139,11 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             const uint4 q = qn;
             fetch();
             uint32_t *Vc = Vs + par * nw * kTM;
-#if GB_SOS_STATIC
             // static predicated loop over the <= 32 state words (n_p <= 1024): no divergent
             // loop, stores independent
 #pragma unroll
             for (int w = 0; w < 32; ++w)
                 if ((zmask >> w) & 1u) Vc[w * kTM + m] = 0u;
-#else
-            for (uint32_t d = zmask; d; d &= d - 1u) Vc[(__ffs(d) - 1) * kTM + m] = 0u;
-#endif
             zmask = 0u;
             rl = 0;
             if (p >= k) { active = false; return; }
@@ -261,11 +251,10 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         bool changed = false;
         bool cyc = true;
         if (epi) {   // incremental A = V^T (bytes, SW128), as in sos_tc2_kernel
-#if GB_SOS_AUPD2
-            // GB_SOS_AUPD2 dirty words per iteration: their state-word loads and expansions
-            // overlap (one word at a time, each store waited on its load: 2.2k cycles per round
+            // four dirty words per iteration: their state-word loads and expansions overlap
+            // (one word at a time, each store waited on its load: 2.2k cycles per round
             // boundary at C2; two at a time 1.8k)
-            constexpr int NA = GB_SOS_AUPD2;
+            constexpr int NA = 4;
             uint32_t d = dirty;
             while (d) {
                 int wq[NA];
@@ -291,23 +280,6 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
                     }
                 }
             }
-#else
-            uint32_t d = dirty;
-            while (d) {
-                const int w = __ffs(d) - 1;
-                d &= d - 1u;
-                const uint32_t wv = (w < nw) ? V[w * kTM + m] : 0u;
-                uint8_t *arow = gbase + P.a_off + (w >> 2) * (kTM * kKB) + m * kKB;
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                    const int ch = 2 * (w & 3) + h2;
-                    const uint32_t bits = (wv >> (h2 * 16)) & 0xffffu;
-                    *reinterpret_cast<uint4 *>(arow + ((ch ^ (m & 7)) * 16)) =
-                        make_uint4(spread4(bits & 15u), spread4((bits >> 4) & 15u),
-                                   spread4((bits >> 8) & 15u), spread4(bits >> 12));
-                }
-            }
-#endif
             dirty = 0u;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }

@@ -490,10 +490,7 @@ sos_tc3x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Sos3Params P
             bool changed = false, cyc = true;
             uint32_t *Vn = Vn2 + (size_t)((rl + 1) & 1) * nw * kTM;
             const uint32_t tl = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-#ifndef GB_TC3_GB
-#define GB_TC3_GB 2
-#endif
-            constexpr int GB = WC < GB_TC3_GB ? WC : GB_TC3_GB;   // TMEM loads in flight per wait
+            constexpr int GB = WC < 2 ? WC : 2;   // TMEM loads in flight per wait (4: spills at WC >= 4)
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
                 const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
                 const uint32_t buf = pc_e % NB;
