@@ -5,6 +5,7 @@ partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l
 SOS pair / streamed-A (incl. Lp = 512 with the state in the global scratch) / 4-warp / generic,
 the cycle-exit flag, and the tensor-core SOM kernel.
 """
+import os
 import sys
 import numpy as np
 import torch
@@ -21,11 +22,14 @@ for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 50
     for i in range(0, k, 5):   # mixed erasure counts (wide-slot / list-mode paths)
         pr[i, rng.choice(c, int(rng.integers(0, c + 1)), replace=False)] = 0xFFFF
     net = gb.Net(c, l)
+    if os.environ.get("SANITIZE_NO_PAIR") == "1":   # racecheck without the CTA-pair kernels
+        net.set_option("sos_pair", 0)
     net.store(torch.from_numpy(msgs.view(np.int16)).cuda())
     net.seal()
     probes = torch.from_numpy(pr.view(np.int16)).cuda()
     for rule in (0, 1, 2):
         net.decode(probes, rule, gamma=2, max_iters=6)
+    net.decode_symbols(probes, 2, gamma=2, max_iters=6)
     net.decode(probes, 0, gamma=0, max_iters=6, flags=gb.FLAG_CYCLE_EXIT)
     if c == 8 and l == 128:
         net.set_option("som_tensor", 1)
