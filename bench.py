@@ -544,6 +544,32 @@ def main():
         ok = (np.array_equal(out_h[0].numpy(), out[0].cpu().numpy()) and
               np.array_equal(out_h[1].numpy(), out[1].cpu().numpy()))
         e2e["matches_device_path"] = bool(ok)
+        # the same step through gb_decode_symbols: the retrieved message (2 B per cluster) comes
+        # back instead of the state bits -- what a host caller that wants the messages copies
+        sym_h = (torch.empty((k, c), dtype=torch.int16).pin_memory(), torch.empty(k, dtype=torch.int16).pin_memory(),
+                 torch.empty(k, dtype=torch.uint8).pin_memory())
+
+        def sym_step():
+            gdist.replicated_store(net, msgs_h)
+            net.decode_symbols(probes_h, rule, gamma=args.gamma, max_iters=args.max_iters, out=sym_h)
+
+        sym_step()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for _ in range(args.e2e_steps):
+            sym_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts = gdist.max_over_ranks([a.elapsed_time(b)], device=dev)[0]
+        e2e["symbols"] = {"value": ws * k * args.e2e_steps / (ts / 1e3), "unit": "probes/s",
+                          "h2d_bytes_per_step": int(my_msgs.nbytes + probes.nbytes),
+                          "d2h_bytes_per_step": int(k * (2 * c + 3)),
+                          "how": "gb_store + gb_seal + gb_decode_symbols with pinned host buffers (the "
+                                 "retrieved message per probe instead of the state bits)",
+                          "matches_iters_status": bool(np.array_equal(sym_h[1].numpy(), out_h[1].numpy()) and
+                                                       np.array_equal(sym_h[2].numpy(), out_h[2].numpy()))}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

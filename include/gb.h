@@ -118,6 +118,7 @@ enum {
 };
 
 #define GB_ERASED 0xFFFFu
+#define GB_AMBIGUOUS 0xFFFEu   /* gb_decode_symbols: several neurons of a cluster active */
 
 /*
  * gb_create -- a network of c clusters with l neurons each (PAPER.md L144-145,
@@ -288,6 +289,27 @@ int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamm
 int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
                  int max_iters, unsigned flags, uint32_t *out_state, uint16_t *out_iters,
                  uint8_t *out_status, void *stream);
+
+/*
+ * gb_decode_symbols -- gb_decode_ex, but instead of the state bits it returns the
+ * retrieved message: for every probe and cluster the index l of the cluster's only
+ * active neuron in the final state, GB_ERASED when no neuron is active and
+ * GB_AMBIGUOUS when several are (the network "retrieves" the
+ * message when one neuron per cluster remains; reading R16: success is
+ * unique exact recovery).  Same decode, rounds and status as gb_decode_ex; only the
+ * output representation differs (2 bytes per cluster instead of the cluster's
+ * padded bits: 16 vs 128 bytes per probe at c=8 l=128, 32 vs 512 at c=16 l=256),
+ * which is what a host-buffer caller copies back over PCIe.
+ *   out_symbols uint16_t[k][c]  row-major; GB_INVALID probes get GB_ERASED rows
+ *   the other arguments, pointer rules (all device or all host; host buffers are
+ *   staged in chunks and the call blocks), errors and concurrency as gb_decode_ex.
+ * Implementation: the decode kernels write the state into call-private scratch
+ * (n_padded/8 bytes per probe, per staged chunk for host buffers) and one pass
+ * maps each cluster block to its symbol.
+ */
+int gb_decode_symbols(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma,
+                      int max_iters, unsigned flags, uint16_t *out_symbols, uint16_t *out_iters,
+                      uint8_t *out_status, void *stream);
 
 /* gb_info -- shape and bookkeeping; any out pointer may be NULL.
  * stored_count counts messages passed to gb_store since create/clear.      */

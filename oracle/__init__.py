@@ -40,6 +40,7 @@ SOS, SOM, HYBRID = 0, 1, 2
 CONVERGED, MAX_ITERS, INVALID, CYCLE = 0, 1, 2, 3
 CYCLE_EXIT = 1   # flag: stop an oscillating SOS probe at V^r == V^{r-2} (N4)
 ERASED = 0xFFFF
+AMBIGUOUS = 0xFFFE
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "gb_oracle.c")
@@ -150,6 +151,19 @@ def unpack_state(state: np.ndarray, c: int, l: int) -> np.ndarray:
     state = np.asarray(state, dtype=np.uint32).reshape(-1, c, wc)
     bits = ((state[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(np.uint8)
     return bits.reshape(state.shape[0], c, wc * 32)[:, :, :l].reshape(state.shape[0], c * l)
+
+
+def symbols(state: np.ndarray, c: int, l: int) -> np.ndarray:
+    """Retrieved message of each final state (R16): per
+    cluster the index of its only active neuron, ERASED when none is active, AMBIGUOUS
+    when several are.  uint16 [K, C].  Plain count over the unpacked 0/1 state."""
+    v = unpack_state(state, c, l).reshape(-1, c, l)
+    out = np.empty(v.shape[:2], dtype=np.uint16)
+    for k in range(v.shape[0]):
+        for cc in range(c):
+            on = np.flatnonzero(v[k, cc])
+            out[k, cc] = ERASED if on.size == 0 else (on[0] if on.size == 1 else AMBIGUOUS)
+    return out
 
 
 def onehot(msgs: np.ndarray, c: int, l: int) -> np.ndarray:

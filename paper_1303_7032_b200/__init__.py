@@ -22,6 +22,7 @@ SUM_OF_SUM, SUM_OF_MAX, HYBRID = 0, 1, 2
 SOS, SOM = SUM_OF_SUM, SUM_OF_MAX
 CONVERGED, MAX_ITERS, INVALID, CYCLE = 0, 1, 2, 3
 FLAG_CYCLE_EXIT = 1   # gb_decode_ex: stop an oscillating sum-of-sum probe at V^r == V^{r-2}
+ERASED, AMBIGUOUS = 0xFFFF, 0xFFFE   # gb_decode_symbols: no / several active neurons in a cluster
 ERASED = 0xFFFF
 GB_OK, GB_EINVAL, GB_ENOMEM, GB_ECUDA, GB_ESTATE, GB_EUNSUPPORTED = 0, -1, -2, -3, -4, -5
 
@@ -31,7 +32,7 @@ LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB:
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_set_option", "gb_get_option", "gb_weights",
            "gb_weights_view", "gb_bits", "gb_or_bits", "gb_pack_upper", "gb_or_upper", "gb_seal", "gb_seal_status",
-           "gb_decode", "gb_decode_ex", "gb_info",
+           "gb_decode", "gb_decode_ex", "gb_decode_symbols", "gb_info",
            "gb_launch_count", "gb_decode_kernel", "gb_last_error", "gb_version")
 
 # gb_set_option keys (include/gb.h GB_OPT_*): kernel choices with identical results
@@ -74,6 +75,7 @@ def lib() -> ctypes.CDLL:
         "gb_or_upper": ([P, P, i64, P], i32),
         "gb_decode": ([P, P, i64, i32, i32, i32, P, P, P, P], i32),
         "gb_decode_ex": ([P, P, i64, i32, i32, i32, ctypes.c_uint, P, P, P, P], i32),
+        "gb_decode_symbols": ([P, P, i64, i32, i32, i32, ctypes.c_uint, P, P, P, P], i32),
         "gb_info": ([P, ctypes.POINTER(i32), ctypes.POINTER(i32), ctypes.POINTER(i32),
                      ctypes.POINTER(i64)], i32),
         "gb_launch_count": ([P, ctypes.POINTER(i64)], i32),
@@ -273,3 +275,26 @@ class Net:
                                   ctypes.c_void_p(_addr(state)), ctypes.c_void_p(_addr(iters)),
                                   ctypes.c_void_p(_addr(status)), _stream(stream)))
         return state, iters, status
+
+    def decode_symbols(self, probes, rule: int, gamma: int = 2, max_iters: int = 20, out=None,
+                       stream=None, flags: int = 0):
+        """gb_decode_symbols: the retrieved message instead of the state bits.  Returns
+        (symbols int16 [K, C] (bit patterns of uint16: l, ERASED or AMBIGUOUS), iters int16 [K],
+        status uint8 [K]) on the probes' side."""
+        k = int(probes.shape[0])
+        assert probes.ndim == 2 and probes.shape[1] == self.c
+        if out is None:
+            if isinstance(probes, np.ndarray):
+                out = (np.empty((k, self.c), np.uint16), np.empty(k, np.uint16), np.empty(k, np.uint8))
+            else:
+                import torch
+                dev = probes.device
+                pin = not probes.is_cuda
+                out = (torch.empty((k, self.c), dtype=torch.int16, device=dev, pin_memory=pin),
+                       torch.empty(k, dtype=torch.int16, device=dev, pin_memory=pin),
+                       torch.empty(k, dtype=torch.uint8, device=dev, pin_memory=pin))
+        sym, iters, status = out
+        _check(lib().gb_decode_symbols(self._h, ctypes.c_void_p(_addr(probes)), k, rule, gamma, max_iters, flags,
+                                       ctypes.c_void_p(_addr(sym)), ctypes.c_void_p(_addr(iters)),
+                                       ctypes.c_void_p(_addr(status)), _stream(stream)))
+        return sym, iters, status

@@ -374,8 +374,11 @@ int gb_decode(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamm
     return gb_decode_ex(net, probes, k, rule, gamma, max_iters, 0u, out_state, out_iters, out_status, stream);
 }
 
-int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
-                 unsigned flags, uint32_t *out_state, uint16_t *out_iters, uint8_t *out_status, void *stream) {
+// gb_decode_ex (out_sym == nullptr: state bits into out_state) and gb_decode_symbols
+// (out_state == nullptr: the state goes to call-private scratch, symbols into out_sym).
+static int decode_impl(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
+                       unsigned flags, uint32_t *out_state, uint16_t *out_sym, uint16_t *out_iters,
+                       uint8_t *out_status, void *stream) {
     if (!net) return fail(GB_EINVAL, "gb_decode: net is NULL");
     if (flags & ~(unsigned)GB_FLAG_CYCLE_EXIT) return fail(GB_EINVAL, "gb_decode: unknown flags 0x%x", flags);
     const int cyc = (rule == GB_SUM_OF_SUM && (flags & GB_FLAG_CYCLE_EXIT)) ? 1 : 0;
@@ -395,17 +398,22 @@ int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int g
         return fail(GB_ESTATE, "gb_decode: the last gb_seal found W8 breaking Eq.(1)'s invariants (%s)",
                     net->seal_msg);
     if (k == 0) return GB_OK;
-    if (!probes || !out_state || !out_iters || !out_status)
+    const bool sym = out_sym != nullptr;
+    void *out_main = sym ? (void *)out_sym : (void *)out_state;
+    if (!probes || !out_main || !out_iters || !out_status)
         return fail(GB_EINVAL, "gb_decode: NULL buffer");
     cudaStream_t st = (cudaStream_t)stream;
-    const int l0 = where(probes, net->device), l1 = where(out_state, net->device),
+    const int l0 = where(probes, net->device), l1 = where(out_main, net->device),
               l2 = where(out_iters, net->device), l3 = where(out_status, net->device);
     if (l0 < 0 || l1 < 0 || l2 < 0 || l3 < 0)
         return fail(GB_EINVAL, "gb_decode: buffer on another device");
     if (l0 && l1 && l2 && l3) {
         gb::Call cl(net, st);
-        GB_CUDA(gb::launch_decode(cl, probes, k, rule, gamma, max_iters, cyc, out_state, out_iters, out_status),
+        uint32_t *state = sym ? cl.alloc_n<uint32_t>((size_t)k * net->s.nw) : out_state;
+        if (!state) return cuda_fail(cl.err, "gb_decode: state scratch");
+        GB_CUDA(gb::launch_decode(cl, probes, k, rule, gamma, max_iters, cyc, state, out_iters, out_status),
                 "gb_decode: launch");
+        if (sym) GB_CUDA(gb::launch_symbols(cl, state, k, out_sym), "gb_decode_symbols: launch");
         return GB_OK;
     }
     if (l0 || l1 || l2 || l3)
@@ -417,9 +425,10 @@ int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int g
     // blocks until done; host-buffer calls on one handle are serialised.
     std::lock_guard<std::mutex> lk(net->stage_mu);
     const size_t pin = (size_t)net->s.C * sizeof(uint16_t);
-    const size_t pout = (size_t)net->s.nw * sizeof(uint32_t) + sizeof(uint16_t) + sizeof(uint8_t);
+    const size_t pout = (size_t)net->s.nw * sizeof(uint32_t) + sizeof(uint16_t) + sizeof(uint8_t) +
+                        (sym ? (size_t)net->s.C * sizeof(uint16_t) : 0);
     const int64_t chunk = std::min<int64_t>(k, 1 << 19);
-    const size_t slot = ((size_t)chunk * (pin + pout) + 255) & ~(size_t)255;
+    const size_t slot = ((size_t)chunk * (pin + pout) + 512 + 255) & ~(size_t)255;
     char *stage = nullptr;
     GB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&stage), 2 * slot, net->pool, st),
             "gb_decode: staging buffer");
@@ -437,14 +446,21 @@ int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int g
         uint32_t *ds = (uint32_t *)(base + (((size_t)chunk * pin + 255) & ~(size_t)255));
         uint16_t *di = (uint16_t *)((char *)ds + (size_t)chunk * net->s.nw * sizeof(uint32_t));
         uint8_t *dt = (uint8_t *)(di + chunk);
+        uint16_t *dy = (uint16_t *)(((uintptr_t)(dt + chunk) + 15) & ~(uintptr_t)15);   // symbols
         cudaError_t e = cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, ss);
         if (e == cudaSuccess) {
             gb::Call cl(net, ss);
             e = gb::launch_decode(cl, dp, n, rule, gamma, max_iters, cyc, ds, di, dt);
         }
+        if (e == cudaSuccess && sym) {
+            gb::Call cl(net, ss);
+            e = gb::launch_symbols(cl, ds, n, dy);
+        }
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
-                                cudaMemcpyDeviceToHost, ss);
+            e = sym ? cudaMemcpyAsync(out_sym + s0 * net->s.C, dy, (size_t)n * net->s.C * sizeof(uint16_t),
+                                      cudaMemcpyDeviceToHost, ss)
+                    : cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
+                                      cudaMemcpyDeviceToHost, ss);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, ss);
         if (e == cudaSuccess) e = cudaMemcpyAsync(out_status + s0, dt, (size_t)n, cudaMemcpyDeviceToHost, ss);
@@ -456,6 +472,21 @@ int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int g
     }
     cudaFreeAsync(stage, st);   // both staging streams are idle now
     return rc;
+}
+
+int gb_decode_ex(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
+                 unsigned flags, uint32_t *out_state, uint16_t *out_iters, uint8_t *out_status, void *stream) {
+    if (!out_state && k > 0) return fail(GB_EINVAL, "gb_decode: NULL buffer");
+    return decode_impl(net, probes, k, rule, gamma, max_iters, flags, out_state, nullptr, out_iters, out_status,
+                       stream);
+}
+
+int gb_decode_symbols(gb_net *net, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters,
+                      unsigned flags, uint16_t *out_symbols, uint16_t *out_iters, uint8_t *out_status,
+                      void *stream) {
+    if (!out_symbols && k > 0) return fail(GB_EINVAL, "gb_decode_symbols: NULL buffer");
+    return decode_impl(net, probes, k, rule, gamma, max_iters, flags, nullptr, out_symbols, out_iters, out_status,
+                       stream);
 }
 
 int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {

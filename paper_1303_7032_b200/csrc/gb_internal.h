@@ -206,5 +206,7 @@ cudaError_t launch_decode_sos_tc(Call &cl, const uint16_t *probes, int64_t k, in
                                  int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
 cudaError_t launch_decode(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma,
                           int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
+// gb_decode_symbols' output pass (gb_symbols.cu): state bits -> one uint16 per cluster
+cudaError_t launch_symbols(Call &cl, const uint32_t *state, int64_t k, uint16_t *out);
 
 }  // namespace gb

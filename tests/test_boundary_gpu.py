@@ -217,3 +217,52 @@ def test_upper_triangle_exchange(gb, c, l, m):
         gb.Net(c, l).pack_upper()                   # not sealed
     for n in (whole, merged):
         n.close()
+
+
+@pytest.mark.parametrize("c,l,m,e,k", [(4, 16, 50, 2, 1000), (8, 128, 5000, 4, 3000), (8, 128, 20000, 4, 1500),
+                                       (16, 256, 30000, 8, 300), (5, 100, 800, 3, 500), (16, 512, 5000, 7, 200)])
+def test_decode_symbols_matches_oracle(gb, c, l, m, e, k):
+    """gb_decode_symbols (the retrieved message per cluster: its only active neuron, or
+    ERASED / AMBIGUOUS) equals the oracle's final state mapped by oracle.symbols, with the
+    same rounds and status, for every rule and kernel family (hyb8, shared-memory, L2, SOS
+    pair / streamed-A); invalid probes give ERASED rows; device buffers."""
+    msgs = gbgen.messages(1000 + c + l, m, c, l)
+    pr, _ = gbgen.probes(1001 + k, msgs, k, e, l, random_count=k // 5)
+    pr[1, 0] = l                                   # invalid symbol
+    w, _ = oracle.store(msgs, c, l)
+    net = gb.Net(c, l)
+    net.store(torch.from_numpy(msgs.view(np.int16)).cuda())
+    net.seal()
+    for rule in (0, 1, 2):
+        sym, it, ss = net.decode_symbols(torch.from_numpy(pr.view(np.int16)).cuda(), rule, gamma=2, max_iters=20)
+        torch.cuda.synchronize()
+        ost, oit, oss = oracle.decode(w, c, l, pr, rule, gamma=2, max_iters=20)
+        want = oracle.symbols(ost, c, l)
+        got = sym.cpu().numpy().view(np.uint16)
+        assert np.array_equal(got, want), (rule, np.flatnonzero((got != want).any(axis=1))[:5])
+        assert np.array_equal(it.cpu().numpy().view(np.uint16), oit) and np.array_equal(ss.cpu().numpy(), oss)
+        assert (got[1] == oracle.ERASED).all() and ss[1].item() == gb.INVALID
+    net.close()
+
+
+def test_decode_symbols_host_buffers_chunked(gb):
+    """gb_decode_symbols with host buffers: 2^19 + 4321 probes (two staged chunks on the two
+    staging streams) equal the device-buffer call and gb_decode's states mapped by
+    oracle.symbols; hybrid (C=8 kernel) and sum-of-sum (CTA pair)."""
+    c, l, m, k = 8, 128, 5000, (1 << 19) + 4321
+    msgs = gbgen.messages(77, m, c, l)
+    pr, _ = gbgen.probes(78, msgs, k, 4, l)
+    net = gb.Net(c, l)
+    net.store(torch.from_numpy(msgs.view(np.int16)).cuda())
+    net.seal()
+    for rule in (2, 0):
+        host = net.decode_symbols(torch.from_numpy(pr.view(np.int16)), rule, gamma=2, max_iters=20)
+        dev = net.decode_symbols(torch.from_numpy(pr.view(np.int16)).cuda(), rule, gamma=2, max_iters=20)
+        st, _, _ = net.decode(torch.from_numpy(pr.view(np.int16)).cuda(), rule, gamma=2, max_iters=20)
+        torch.cuda.synchronize()
+        for a, b in zip(host, dev):
+            assert np.array_equal(a.numpy(), b.cpu().numpy())
+        idx = np.arange(0, k, 997)
+        want = oracle.symbols(st.cpu().numpy().view(np.uint32)[idx], c, l)
+        assert np.array_equal(host[0].numpy().view(np.uint16)[idx], want)
+    net.close()

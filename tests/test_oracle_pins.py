@@ -570,3 +570,28 @@ def test_work_counter_closed_forms(c, l):
             assert (blk == c - e + e * l).all() and (it == 2).all()
             _, it, _, blk = oracle.decode(w0, c, l, pr, HYBRID, gamma=1, with_blocks=True)
             assert (blk == (c - e) * e).all() and (it == 1).all()
+
+
+# ---------------------------------------------------------------- retrieved message (symbols)
+def test_symbols_of_onehot_and_ensembles():
+    """oracle.symbols (the retrieved message; R16): a one-hot
+    state of message m maps back to m exactly (PAPER.md L146-147 encoding), an empty
+    cluster to ERASED, a cluster with two active neurons to AMBIGUOUS -- including
+    padding-adjacent neurons at a ragged L."""
+    for c, l in ((4, 16), (8, 128), (3, 3), (5, 100)):
+        msgs = gbgen.messages(3, 50, c, l)
+        wc = oracle.words_per_cluster(l)
+        st = np.zeros((50, c * wc), np.uint32)
+        for k in range(50):
+            for cc in range(c):
+                s = int(msgs[k, cc])
+                st[k, cc * wc + s // 32] |= np.uint32(1 << (s % 32))
+        assert np.array_equal(oracle.symbols(st, c, l), msgs)
+        assert np.array_equal(oracle.unpack_state(st, c, l), oracle.onehot(msgs, c, l))
+        st2 = st.copy()
+        st2[0, :wc] = 0                                   # cluster 0 of probe 0 empty
+        s1 = (int(msgs[1, 0]) + 1) % l                    # a second neuron in cluster 0 of probe 1
+        st2[1, s1 // 32] |= np.uint32(1 << (s1 % 32))
+        sym = oracle.symbols(st2, c, l)
+        assert sym[0, 0] == oracle.ERASED and sym[1, 0] == oracle.AMBIGUOUS
+        assert np.array_equal(sym[2:], msgs[2:]) and np.array_equal(sym[0, 1:], msgs[0, 1:])
