@@ -152,8 +152,10 @@ int gb_create(int c, int l, int device, gb_net **out) {
     net->sm_count = prop.multiProcessorCount;
     for (int o = 0; o < gb::kNumOptions; ++o) net->opt[o].store(gb::option_default(o));
     const size_t w8b = (size_t)s.np * s.np, wbb = (size_t)s.np * s.nw * sizeof(uint32_t);
+    // Wb and, behind it, the cluster unions Wu (C x C blocks, seal_kernel's companion)
+    const size_t wub = 2 * (size_t)s.C * s.C * s.Wc * sizeof(uint32_t);
     void *hs = nullptr;
-    if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb) != cudaSuccess ||
+    if (cudaMalloc(&net->w8, w8b) != cudaSuccess || cudaMalloc(&net->wb, wbb + wub) != cudaSuccess ||
         cudaMalloc(&net->dcount, 32) != cudaSuccess ||
         cudaHostAlloc(&hs, sizeof(gb::Status), cudaHostAllocMapped) != cudaSuccess) {
         cudaGetLastError();
@@ -170,7 +172,8 @@ int gb_create(int c, int l, int device, gb_net **out) {
     cudaError_t e = cudaHostGetDevicePointer(&hd, hs, 0);
     net->hstat_dev = static_cast<gb::Status *>(hd);
     cudaMemset(net->w8, 0, w8b);
-    cudaMemset(net->wb, 0, wbb);
+    cudaMemset(net->wb, 0, wbb + wub);
+    net->wu = net->wb + (size_t)s.np * s.nw;
     net->dflag = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(net->dcount) + 8);
     cudaMemset(net->dcount, 0, 32);
     for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&net->stage_stream[i], cudaStreamNonBlocking);

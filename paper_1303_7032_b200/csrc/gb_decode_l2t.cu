@@ -98,7 +98,8 @@ __global__ void __launch_bounds__(NT, 1)
 decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int T,
                   uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
                   uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
-                  unsigned long long *__restrict__ ovf_count, uint32_t *__restrict__ xscratch) {
+                  unsigned long long *__restrict__ ovf_count, uint32_t *__restrict__ xscratch,
+                  const uint32_t *__restrict__ wu) {
     constexpr int LP = 32 * WC;
     // rows per push stage = one word group of G words (the lowest remaining candidate of each),
     // all G loads predicated and in flight together; groups are visited cyclically until the
@@ -154,6 +155,9 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
         // ([word][thread], L2): only the current state is read in the push loops, so shared
         // memory holds one copy and twice as many threads fit (latency hiding of the L2 rows)
         uint32_t *X = sm, *Xn = xscratch + (size_t)blockIdx.x * MAXS * WC * NT;
+        // bit t set <=> slot t holds every real neuron of its cluster: a push from it covers
+        // exactly the cluster union Wu (one block load instead of ~L/4 rows; seal builds Wu)
+        uint32_t fullm = 0u;
         // ---- a5 prune (hybrid) / init (SOM)
         if (RULE == GB_HYBRID) {
             uint32_t x[MAXS][WC];
@@ -178,15 +182,22 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
             }
 #pragma unroll
             for (int t = 0; t < MAXS; ++t)
-                if (t < nslot)
+                if (t < nslot) {
+                    bool full = true;
 #pragma unroll
-                    for (int u = 0; u < WC; ++u) X[(t * WC + u) * NT + tid] = x[t][u];
+                    for (int u = 0; u < WC; ++u) {
+                        X[(t * WC + u) * NT + tid] = x[t][u];
+                        full &= x[t][u] == rmask[u];
+                    }
+                    if (full) fullm |= 1u << t;
+                }
         } else {
             for (int t = 0; t < nslot; ++t) {
                 const int c = slot_c(t);
                 if ((emask >> c) & 1u) {
 #pragma unroll
                     for (int u = 0; u < WC; ++u) X[(t * WC + u) * NT + tid] = rmask[u];
+                    fullm |= 1u << t;
                 } else {
                     const unsigned sym = __ldg(pr + c);
 #pragma unroll
@@ -202,6 +213,7 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
         } else {
             while (it < T) {
                 bool changed = false;
+                uint32_t fulln = fullm;   // the round's pushes read the old state: update after it
                 for (int t = 0; t < nslot; ++t) {
                     const int ct = slot_c(t);
                     uint32_t alive[WC];
@@ -225,6 +237,10 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
 #pragma unroll
                         for (int u = 0; u < WC; ++u) h[u] = 0u;
                         uint32_t miss = 1u;
+                        if ((fullm >> si) & 1u) {   // full source cluster: H = Wu[c_si][c_t]
+                            ldg_block<WC>(wu + (size_t)(slot_c(si) * C + ct) * WC, h);
+                            left = 0u;
+                        }
                         while (miss && left) {
 #pragma unroll
                             for (int grp = 0; grp < WC / G; ++grp) {
@@ -264,8 +280,10 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                     for (int u = 0; u < WC; ++u) {
                         changed |= (alive[u] != X[(t * WC + u) * NT + tid]);
                         Xn[(t * WC + u) * NT + tid] = alive[u];
+                        if (alive[u] != rmask[u]) fulln &= ~(1u << t);
                     }
                 }
+                fullm = fulln;
                 if (changed)
                     for (int w = 0; w < nslot * WC; ++w) X[w * NT + tid] = Xn[w * NT + tid];
                 ++it;
@@ -321,7 +339,7 @@ cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int max_iters,
     int64_t grid = (k + NT - 1) / NT;
     if (grid > net->sm_count) grid = net->sm_count;
     fn<<<(unsigned)grid, NT, smem, cl.st>>>(net->s, net->wb, probes, k, max_iters, state, iters, status, ovf,
-                                            cnt + 1, xscratch);
+                                            cnt + 1, xscratch, wu_of(net, net->seal_gen));
     cl.launched();
     return cudaGetLastError();
 }

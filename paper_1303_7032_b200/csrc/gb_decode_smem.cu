@@ -69,7 +69,8 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                    int64_t k, int T, uint32_t *__restrict__ out_state,
                    uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status,
                    const int64_t *__restrict__ list, const unsigned long long *__restrict__ list_count,
-                   int64_t *__restrict__ ovf, unsigned long long *__restrict__ ovf_count) {
+                   int64_t *__restrict__ ovf, unsigned long long *__restrict__ ovf_count,
+                   const uint32_t *__restrict__ wu) {
     extern __shared__ __align__(16) uint32_t smem[];
     constexpr int LP = 32 * WC;
     constexpr int BB = 4 * WC;                      // bytes per block
@@ -160,6 +161,9 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         uint32_t ra[kMaxC];
         // bit t*WC+u set <=> word u of slot t is non-zero (lets the push skip empty words)
         uint32_t nzall = 0u;
+        // bit t set <=> slot t holds every real neuron of its cluster (MAXS = 8 instance): a push
+        // from it covers exactly the cluster union Wu (one load; seal builds Wu)
+        uint32_t fullm = 0u;
         // 4-slot instance: the slot states live in registers (static slot indices)
         uint32_t xr[MAXS == 4 ? 4 : 1][WC];
         unsigned nk = 0;
@@ -199,12 +203,15 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
 #pragma unroll
                     for (int u = 0; u < WC; ++u) x[u] = ((sc >> 5) == (unsigned)u) ? (1u << (sc & 31)) : 0u;
                 }
+                bool full = true;
 #pragma unroll
                 for (int u = 0; u < WC; ++u) {
                     if constexpr (MAXS == 4) xr[t][u] = x[u];
                     else X[(t * WC + u) * NT + tid] = x[u];
                     if (x[u]) nzall |= 1u << (t * WC + u);
+                    full &= x[u] == real_mask_u(s.L, u);
                 }
+                if (full) fullm |= 1u << t;
             }
         }
 
@@ -314,6 +321,12 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             for (int u = 0; u < WC; ++u) h[u] = 0u;
                             uint32_t miss = any;
                             const uint32_t ckey = (uint32_t)c;
+                            if ((fullm >> sidx) & 1u) {   // full source cluster: H = Wu[c2][c]
+                                const uint32_t *ub = wu + (size_t)(c2 * C + c) * WC;
+#pragma unroll
+                                for (int u = 0; u < WC; ++u) h[u] = __ldg(ub + u);
+                                miss = 0u;
+                            }
                             // one loop over the source's candidate words (a lane that runs out of
                             // word u2 moves on inside the same loop: no per-word divergent tails)
                             const uint32_t *xs = X + (sidx * WC) * NT + tid;
@@ -365,6 +378,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             changed |= (*a != xn[t][u]);
                             *a = xn[t][u];
                             if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
+                            if (xn[t][u] != real_mask_u(s.L, u)) fullm &= ~(1u << t);
                         }
                     }
                 }
@@ -436,7 +450,7 @@ cudaError_t launch_t(Call &cl, const uint16_t *probes, int64_t k, int max_iters,
     int64_t grid = list ? net->sm_count : (k + NT - 1) / NT;
     if (grid > net->sm_count) grid = net->sm_count;
     fn<<<(unsigned)grid, NT, smem, cl.st>>>(s, net->wb, probes, k, max_iters, state, iters, status, list, list_count,
-                                            ovf, ovf_count);
+                                            ovf, ovf_count, wu_of(net, net->seal_gen));
     cl.launched();
     return cudaGetLastError();
 }

@@ -66,6 +66,9 @@ struct gb_net {
     int sm_count;
     uint8_t *w8;          // [np][np] u8, row-major
     uint32_t *wb;         // [np][nw] bit rows
+    uint32_t *wu;         // 2 x [C][C][Wc] cluster unions: block t of the OR of all rows of cluster
+                          // s (the push cover of a full source cluster), built by the seal into
+                          // buffer (generation & 1) -- wu_of(net, net->seal_gen) is the current one
     // Device status words (one 32-byte allocation):
     //   [0, 8) invalid stored messages since create/clear (store kernels; reset by gb_clear)
     //   [8, 12) structural error flags of the running seal, [12, 16) its edge count,
@@ -109,6 +112,10 @@ struct gb_net {
 };
 
 namespace gb {
+
+inline uint32_t *wu_of(const gb_net *net, unsigned long long gen) {
+    return net->wu + (size_t)(gen & 1ull) * net->s.C * net->s.C * net->s.Wc;
+}
 
 // One store / decode call: the caller's stream and the call's private device scratch,
 // allocated stream-ordered from the handle's memory pool and released (stream-ordered)

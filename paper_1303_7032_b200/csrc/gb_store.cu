@@ -75,9 +75,15 @@ __device__ __forceinline__ uint32_t pack32(const uint8_t *p, unsigned &nonbin) {
     return bits;
 }
 
+// Also builds the cluster unions Wu[s][t] = OR over the rows j of cluster s of block t of
+// row j: the cover H that a push from a source whose candidate set is the whole cluster
+// computes (the sum-of-max state of an erased cluster before its first round, PAPER.md
+// L270-271), which the bit kernels then read in one load instead of ~L/4 row loads.  Each
+// tile's warp ORs its 32 packed words into Wu (two buffers alternating by seal generation:
+// this seal ORs into `wu` and zeroes `wu_next` for the next one).
 __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *__restrict__ wb,
                             unsigned long long *__restrict__ dcount, Status *__restrict__ hstat,
-                            unsigned long long gen) {
+                            unsigned long long gen, uint32_t *__restrict__ wu, uint32_t *__restrict__ wu_next) {
     unsigned *dflag = reinterpret_cast<unsigned *>(dcount + 1);   // [0] flags, [1] edges, [2] CTAs done
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -107,6 +113,12 @@ __global__ void seal_kernel(Shape s, const uint8_t *__restrict__ w8, uint32_t *_
         if (lane == 0 && anybad) atomicOr(dflag, anybad);
         const unsigned ne = __reduce_add_sync(0xffffffffu, (unsigned)__popc(P));   // edges (both directions)
         if (lane == 0 && ne) atomicAdd(dflag + 1, ne);
+        const unsigned un = __reduce_or_sync(0xffffffffu, P);                        // cluster union
+        if (lane == 0 && un) atomicOr(wu + (ci * s.C + cj) * s.Wc + (tj - cj * s.Wc), un);
+    }
+    {
+        const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (t < (int64_t)s.C * s.C * s.Wc) wu_next[t] = 0u;
     }
     // the last CTA to finish publishes the status to mapped host memory (no host sync in
     // gb_seal) and resets the per-seal words for the next seal
@@ -404,8 +416,11 @@ cudaError_t launch_seal(gb_net *net, cudaStream_t st) {
     const int64_t warps = (int64_t)(net->s.np / 32) * (net->s.np / 32);
     const int block = 256;
     const int64_t grid = (warps * 32 + block - 1) / block;
-    seal_kernel<<<(unsigned)grid, block, 0, st>>>(net->s, net->w8, net->wb, net->dcount, net->hstat_dev,
-                                                  net->seal_gen);
+    const int64_t zthreads = (int64_t)net->s.C * net->s.C * net->s.Wc;   // wu_next zeroing
+    const int64_t g2 = std::max<int64_t>(grid, (zthreads + block - 1) / block);
+    seal_kernel<<<(unsigned)g2, block, 0, st>>>(net->s, net->w8, net->wb, net->dcount, net->hstat_dev,
+                                                net->seal_gen, wu_of(net, net->seal_gen),
+                                                wu_of(net, net->seal_gen + 1));
     net->launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
 }
