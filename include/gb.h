@@ -94,14 +94,17 @@ enum {
                                   general shared-memory hybrid kernel               */
     GB_OPT_L2T = 4,            /* 1 (default): thread-per-probe L2 bit kernel; 0:
                                   warp-per-probe kernel (W rows beyond shared mem)   */
-    GB_OPT_HYB8_SPLIT = 5,     /* -1 (default): choose the C = 8 hybrid kernel's
-                                  push variant by W's density (known once a seal's
-                                  status reached the host): staged when dense (>0.65),
-                                  a uniform loop when sparse; 0 (loop) / 1 (staged)
-                                  force it (bit-exact either way)                   */
-    GB_OPT_STORE_SCATTER = 6   /* 1: gb_store with scattered byte writes only;
+    GB_OPT_HYB8_SPLIT = 5,     /* -1 (default): choose the C = 8 hybrid kernel by
+                                  W's density (known once a seal's status reached
+                                  the host): the rotated-layout kernel when dense
+                                  (>0.65), the uniform-loop kernel when sparse;
+                                  0 (loop) / 1 (rotated) force it (bit-exact)        */
+    GB_OPT_STORE_SCATTER = 6,  /* 1: gb_store with scattered byte writes only;
                                   0 (default): shared-memory privatised tiles for
                                   large batches                                      */
+    GB_OPT_HYB8_ROWS = 7       /* 0 (default): rows of the rotated-layout hybrid
+                                  kernel's first push step chosen by W's density;
+                                  5..8 force it (bit-exact either way)               */
 };
 
 /* gb_decode_ex flags. */
@@ -156,7 +159,8 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
 
 /*
  * gb_set_option / gb_get_option -- per-handle kernel selection (GB_OPT_*).
- * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1).  GB_EINVAL for an unknown
+ * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1; GB_OPT_HYB8_ROWS 0 or 5..8).
+ * GB_EINVAL for an unknown
  * option or value.  Not to be called while decodes on the handle run.
  */
 int gb_set_option(gb_net *net, int option, int value);

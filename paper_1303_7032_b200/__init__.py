@@ -37,7 +37,7 @@ EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_set_option", "
 
 # gb_set_option keys (include/gb.h GB_OPT_*): kernel choices with identical results
 OPTIONS = {"sos_pair": 0, "sos_streamed": 1, "som_tensor": 2, "hyb8": 3, "l2t": 4, "hyb8_split": 5,
-           "store_scatter": 6}
+           "store_scatter": 6, "hyb8_rows": 7}
 
 _lib = None
 
@@ -129,7 +129,8 @@ class Net:
     """One GBNN network on one CUDA device (gb_net handle).
 
     ``options``: kernel-selection options (``OPTIONS`` keys -> 0/1, ``hyb8_split``
-    also -1), passed to gb_set_option; they pick between bit-exact kernels."""
+    also -1, ``hyb8_rows`` 0 or 5..8), passed to gb_set_option; they pick between
+    bit-exact kernels."""
 
     def __init__(self, c: int, l: int, device: int = 0, **options):
         h = ctypes.c_void_p()

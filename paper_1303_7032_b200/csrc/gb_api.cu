@@ -222,17 +222,22 @@ int gb_destroy(gb_net *net) {
 
 int gb_set_option(gb_net *net, int option, int value) {
     if (!net) return fail(GB_EINVAL, "gb_set_option: net is NULL");
-    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_STORE_SCATTER)
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_HYB8_ROWS)
         return fail(GB_EINVAL, "gb_set_option: unknown option %d", option);
-    const int lo = option == GB_OPT_HYB8_SPLIT ? -1 : 0;
-    if (value < lo || value > 1) return fail(GB_EINVAL, "gb_set_option: value %d outside [%d, 1]", value, lo);
+    if (option == GB_OPT_HYB8_ROWS) {
+        if (value != 0 && (value < 5 || value > 8))
+            return fail(GB_EINVAL, "gb_set_option: value %d not 0 or 5..8", value);
+    } else {
+        const int lo = option == GB_OPT_HYB8_SPLIT ? -1 : 0;
+        if (value < lo || value > 1) return fail(GB_EINVAL, "gb_set_option: value %d outside [%d, 1]", value, lo);
+    }
     net->opt[option].store(value);
     return GB_OK;
 }
 
 int gb_get_option(gb_net *net, int option, int *value) {
     if (!net || !value) return fail(GB_EINVAL, "gb_get_option: NULL argument");
-    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_STORE_SCATTER)
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_HYB8_ROWS)
         return fail(GB_EINVAL, "gb_get_option: unknown option %d", option);
     *value = net->opt[option].load();
     return GB_OK;

@@ -8,10 +8,10 @@
 //    in ingest, prune and output;
 //  * the push of one (source -> target) pair reads candidate rows several at a
 //    time instead of walking the source's bits one at a time: when W is dense
-//    in stages (the lowest candidate of every non-empty word of the source, then
-//    the highest other candidate of every word in two halves, then the rest one
-//    at a time), when sparse in a loop of "the lowest remaining candidate of
-//    every word"; each step runs only while some target candidate is still
+//    (decode_hyb8r_kernel) one row per 16-neuron half-word of the source, in a
+//    shared-memory layout where those loads never bank-conflict; when sparse
+//    (decode_hyb8_kernel) a loop of "the lowest remaining candidate of every
+//    word"; each step runs only while some target candidate is still
 //    uncovered (bail-out-early), and every source candidate is read
 //    at most once, so the cover H is the same OR of rows;
 //  * output through a TMA tensor store: each warp writes its 32 probes'
@@ -61,34 +61,14 @@ __device__ __forceinline__ void lds4p(uint32_t p, uint32_t a, uint32_t (&v)[4]) 
         : "r"(p), "r"(a));
 }
 __device__ __forceinline__ uint32_t lowbit(uint32_t x) { return __ffs(x) - 1; }
-__device__ __forceinline__ uint32_t highbit(uint32_t x) { return 31 - __clz(x); }
-// Two push variants, chosen by W's density (seal counts the edges):
-//  DENSE (density > 0.65): stage 1 = the lowest candidate row of each word of the source;
-//    stage 2 = the highest other candidate of each word, in two halves with a cover check
-//    between them (at C3 ~32 candidates per erased cluster: stage 1 covers ~77% of the pairs and
-//    two more rows usually cover the rest); stage 3 = the remaining rows one at a time;
-//  sparse: one loop whose every step reads the lowest remaining candidate row of each word (up to
-//    4 loads in flight) until the target is covered or the source exhausted -- few candidates per
-//    cluster, many of them dying, so the uniform loop wastes fewer warp slots than the stages.
-// Same-box A/B (round 2, 10^7 probes, hybrid, c=8 l=128): M=5k (density 0.26) 2.24 -> 1.74 ms
-// with the loop, M=10k (0.46) 4.11 -> 3.32, M=15k (0.60) 1.19 -> 1.08; the staged form stays
-// faster when dense: M=20k (C3, 0.70) 0.960 vs 0.973, M=30k (0.84) 0.855 vs 0.870.  A third form,
-// stage 1 then one "pull" row per uncovered target candidate (row i's block of the source meets
-// the source's remaining candidates, W symmetric), was slower at every density (C3 1.12 ms,
-// M=5k 2.11): its loads run on few lanes, so each costs almost a full wavefront.
-//
-// The kernel is bound by the LSU data pipe (~87% of one shared-memory wavefront per SM per clock
-// at C3); half of its wavefronts are bank conflicts, because a row block sits in the bank group of
-// its target cluster and the 8 lanes of a quarter-warp target random clusters.  Measured and not
-// kept (round 2, same-box A/B at C3):
-//  * unpredicated stage loads (empty words read a discarded row, fixed up in a rare branch):
-//    11% fewer instructions, ALU pipe 71% -> 55%, but 0.961 vs 0.931 ms -- not ALU-bound;
-//  * a conflict-free probe order: each CTA classifies its 768-probe chunk by erasure set and
-//    places 4 probes erasing E and 4 erasing ~E on every quarter-warp (counting sort in shared
-//    memory, CTA-wide staging of the output rows): conflicts 118M -> 51M per launch, but 1.15 ms
-//    (three CTA barriers per chunk and the exposed probe loads: long-scoreboard and barrier
-//    stalls).  Host-side ordering of the same probes (no in-kernel cost) gives 0.88 vs 0.97 ms.
-template <bool DENSE>
+// Sparse W (density <= 0.65, counted by seal): one loop whose every step reads the lowest
+// remaining candidate row of each word (up to 4 loads in flight) until the target is covered or
+// the source exhausted -- few candidates per cluster, many of them dying.  W in row-major order
+// (a row block lies in the bank group of its target cluster).  Same-box A/B (round 2, 10^7
+// probes, hybrid, c=8 l=128): M=5k (density 0.26) 2.24 -> 1.74 ms with the loop instead of the
+// round-1 stages, M=10k (0.46) 4.11 -> 3.32, M=15k (0.60) 1.19 -> 1.08; the rotated-layout kernel
+// below is slower there (M=5k 2.48, M=10k 4.98, M=15k 1.09 ms): with ~2-17 candidates per
+// erased cluster most of its 8 half-word loads are empty.
 __global__ void __launch_bounds__(kNT, 1)
 decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
                    int T, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
@@ -249,99 +229,29 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
                                 // block c_t of row (c2, 32u + b): rb + (32u + b) * 128
                                 const uint32_t rb = w_s + ((slots >> (4 * sidx)) & 15u) * kClusterB + (ct << 4);
                                 uint32_t h[4] = {0u, 0u, 0u, 0u};
-                                if constexpr (!DENSE) {
-                                    // sparse: the lowest remaining candidate row of every word per
-                                    // step (4 loads in flight) until covered or exhausted
-                                    uint32_t rem[4];
+                                // sparse: the lowest remaining candidate row of every word per
+                                // step (4 loads in flight) until covered or exhausted
+                                uint32_t rem[4];
 #pragma unroll
-                                    for (int u = 0; u < 4; ++u) rem[u] = xr[sidx][u];
-                                    uint32_t miss;
-                                    do {
-                                        uint32_t r[4][4];
+                                for (int u = 0; u < 4; ++u) rem[u] = xr[sidx][u];
+                                uint32_t miss;
+                                do {
+                                    uint32_t r[4][4];
 #pragma unroll
-                                        for (int u = 0; u < 4; ++u) {
-                                            const uint32_t x = rem[u];
+                                    for (int u = 0; u < 4; ++u) {
+                                        const uint32_t x = rem[u];
 #pragma unroll
-                                            for (int v = 0; v < 4; ++v) r[u][v] = 0u;
-                                            lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
-                                            rem[u] = x & (x - 1u);
-                                        }
-                                        miss = 0u;
-#pragma unroll
-                                        for (int v = 0; v < 4; ++v) {
-                                            h[v] |= (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
-                                            miss |= alive[v] & ~h[v];
-                                        }
-                                    } while (miss && ((rem[0] | rem[1]) | (rem[2] | rem[3])));
-                                } else {
-                                    // stage 1: the lowest candidate of each non-empty word, in flight
-                                    // together
-                                    {
-                                        uint32_t r[4][4];
-#pragma unroll
-                                        for (int u = 0; u < 4; ++u) {
-                                            const uint32_t x = xr[sidx][u];
-#pragma unroll
-                                            for (int v = 0; v < 4; ++v) r[u][v] = 0u;
-                                            lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
-                                        }
-#pragma unroll
-                                        for (int v = 0; v < 4; ++v) h[v] = (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+                                        for (int v = 0; v < 4; ++v) r[u][v] = 0u;
+                                        lds4p(x, rb + (u * 32 + lowbit(x)) * kRowB, r[u]);
+                                        rem[u] = x & (x - 1u);
                                     }
-                                    uint32_t miss = 0u;
+                                    miss = 0u;
 #pragma unroll
-                                    for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                    if (miss) {
-                                        // stage 2: the highest other candidate of each word holding
-                                        // >= 2, words 0-1, a cover check, then words 2-3 (the loads of
-                                        // a half predicated and in flight together)
-#pragma unroll
-                                        for (int g = 0; g < 2; ++g) {
-                                            if (g == 1) {
-                                                miss = 0u;
-#pragma unroll
-                                                for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                                if (!miss) break;
-                                            }
-                                            uint32_t r[2][4];
-#pragma unroll
-                                            for (int uu = 0; uu < 2; ++uu) {
-                                                const int u = 2 * g + uu;
-                                                const uint32_t x = xr[sidx][u];
-                                                const uint32_t x2 = x & (x - 1u);
-#pragma unroll
-                                                for (int v = 0; v < 4; ++v) r[uu][v] = 0u;
-                                                lds4p(x2, rb + (u * 32 + highbit(x2)) * kRowB, r[uu]);
-                                            }
-#pragma unroll
-                                            for (int v = 0; v < 4; ++v) h[v] |= r[0][v] | r[1][v];
-                                        }
-                                        miss = 0u;
-#pragma unroll
-                                        for (int v = 0; v < 4; ++v) miss |= alive[v] & ~h[v];
-                                        if (miss) {
-                                            // stage 3: the rest, one row at a time
-#pragma unroll
-                                            for (int u = 0; u < 4; ++u) {
-                                                const uint32_t x = xr[sidx][u];
-                                                uint32_t rem = x & (x - 1u);                   // minus stage 1
-                                                if (rem) rem &= ~(1u << highbit(rem));         // minus stage 2
-                                                while (rem && miss) {
-                                                    const uint32_t b = lowbit(rem);
-                                                    rem &= rem - 1u;
-                                                    uint32_t r[4];
-                                                    lds4(rb + (u * 32 + b) * kRowB, r);
-                                                    miss = 0u;
-#pragma unroll
-                                                    for (int v = 0; v < 4; ++v) {
-                                                        h[v] |= r[v];
-                                                        miss |= alive[v] & ~h[v];
-                                                    }
-                                                }
-                                            }
-                                        }
+                                    for (int v = 0; v < 4; ++v) {
+                                        h[v] |= (r[0][v] | r[1][v]) | (r[2][v] | r[3][v]);
+                                        miss |= alive[v] & ~h[v];
                                     }
-                                }
+                                } while (miss && ((rem[0] | rem[1]) | (rem[2] | rem[3])));
                                 any = 0u;
 #pragma unroll
                                 for (int v = 0; v < 4; ++v) {
@@ -412,6 +322,288 @@ decode_hyb8_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__
     if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// ---- rotated-layout kernel (dense W) ------------------------------------------------------------
+// The push reads one row per 16-neuron half-word of the source's candidates (8 rows per pair, in
+// flight together; at C3 ~32 candidates per erased cluster, so the 8 rows cover the target in
+// ~99.8% of the pairs and the rest are read one at a time).  W is laid out in shared memory so
+// that those 8 loads never conflict: row i's block t sits in 16-byte chunk (i >> 4) of its line,
+//   addr(c, i, t) = c * 17 KiB + ((i & 15) + 1) * 1 KiB + t * 128 + (i >> 4) * 16,
+// i.e. the bank group of a row block is the half-word its neuron lies in, whatever the target.
+// Lane q (= lane & 7) issues half-word (k + q) & 7 as its k-th load, so the 8 lanes of a
+// quarter-warp always hit 8 different bank groups.  Group 0 of every cluster is zero: an empty
+// half-word reads it (address offset __ffs(0) = 0), so the loads need no predicate and no zeroed
+// destination registers.  The prune's loads (known rows) keep random bank groups.
+constexpr int kGrpB = 1024;                  // one (cluster, i & 15) group: 8 lines of 128 B
+constexpr int kClusterBr = 17 * kGrpB;       // group 0 = zeros, groups 1..16 = i & 15 = 0..15
+constexpr int kNTr = 512;                    // threads per CTA (one probe each)
+constexpr int kWarpsR = kNTr / 32;
+constexpr size_t kSmemR = 1024 + 8 * (size_t)kClusterBr + (size_t)kWarpsR * kStageB;
+
+template <int NR>
+__global__ void __launch_bounds__(kNTr, 1)
+decode_hyb8r_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes, int64_t k, int L,
+                    int T, const __grid_constant__ CUtensorMap omap, uint16_t *__restrict__ out_iters,
+                    uint8_t *__restrict__ out_status, int64_t *__restrict__ ovf,
+                    unsigned long long *__restrict__ ovf_count) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    const uint32_t sbase = ((uint32_t)__cvta_generic_to_shared(smem_raw) + 1023u) & ~1023u;
+    const uint32_t w_s = sbase;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t stg = w_s + 8 * kClusterBr + warp * kStageB;   // 1024-aligned (128-B swizzle)
+    const uint32_t my_row = stg + lane * 128;
+    const uint32_t sw = (uint32_t)(lane & 7);
+
+    // W bit rows -> shared memory in the rotated layout: smem chunk g = (c, group, t, chunk),
+    // consecutive threads store consecutive chunks (conflict-free)
+    for (int g = tid; g < 8 * (kClusterBr / 16); g += kNTr) {
+        const int c = g / (kClusterBr / 16), rest = g - c * (kClusterBr / 16), grp = rest >> 6;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (grp) {
+            const int i = (rest & 7) * 16 + grp - 1, t = (rest >> 3) & 7;
+            v = __ldg(reinterpret_cast<const uint4 *>(wb) + ((c * 128 + i) * 8 + t));
+        }
+        sts4(w_s + g * 16, v.x, v.y, v.z, v.w);
+    }
+    __syncthreads();
+    uint32_t rmask[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int nb = min(32, max(0, L - u * 32));
+        rmask[u] = nb == 32 ? 0xffffffffu : ((1u << nb) - 1u);
+    }
+    // lane constants of the source rotation: the k-th load reads half-word (k + q) & 7
+    const uint32_t q = (uint32_t)(lane & 7);
+    const bool rot1 = (q >> 1) & 1u, rot2 = (q >> 2) & 1u;
+    const uint32_t rots = (q & 1u) * 16u;
+    const uint32_t q16 = q << 4;
+    auto qk = [&](int kk) { return (q16 + 16u * (uint32_t)kk) & 0x70u; };   // chunk of rotated half-word kk
+
+    const int64_t stride = (int64_t)gridDim.x * kNTr;
+    int64_t pb = ((int64_t)blockIdx.x * kWarpsR + warp) * 32;
+    uint4 qnext = make_uint4(0u, 0u, 0u, 0u);
+    if (pb + lane < k) qnext = __ldg(reinterpret_cast<const uint4 *>(probes + (pb + lane) * 8));
+    for (; pb < k; pb += stride) {
+        const int64_t p = pb + lane;
+        // ---- a1 ingest (the next batch's probe is loaded one batch ahead)
+        const uint32_t w4[4] = {qnext.x, qnext.y, qnext.z, qnext.w};
+        if (p + stride < k) qnext = __ldg(reinterpret_cast<const uint4 *>(probes + (p + stride) * 8));
+        auto sym = [&](int c) { return (w4[c >> 1] >> (16 * (c & 1))) & 0xffffu; };
+        uint32_t emask = 0, bad = 0, live = 0;
+        if (p < k) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (sym(c) == kErased) emask |= 1u << c;
+                else if (sym(c) >= (uint32_t)L) bad = 1;
+            }
+            live = 1;
+        }
+        const uint32_t nslot = __popc(emask);
+        if (live && !bad && nslot > 4) {   // needs more slots: decoded by decode_smem_kernel (list mode)
+            ovf[atomicAdd(ovf_count, 1ull)] = p;
+            live = 0;
+        }
+        const bool work = live && !bad;
+        uint32_t slots = 0;   // erased clusters ascending, 4 bits each
+        {
+            uint32_t em = emask;
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (em) {
+                    slots |= (uint32_t)(__ffs(em) - 1) << (4 * t);
+                    em &= em - 1u;
+                }
+            }
+        }
+        // ---- a5 prune: X^0_c = AND over known clusters kc of block c of row (kc, p_kc)
+        uint32_t xr[4][4];
+        {
+            uint32_t ra[8];
+            uint32_t km = (~emask) & 0xffu;
+            const uint64_t sp_lo = ((uint64_t)w4[1] << 32) | w4[0], sp_hi = ((uint64_t)w4[3] << 32) | w4[2];
+            auto next_row = [&]() {
+                const uint32_t kc = km ? (uint32_t)(__ffs(km) - 1) : 0u;
+                km &= km - 1u;
+                const uint32_t sk = (uint32_t)(((kc < 4) ? sp_lo : sp_hi) >> (16 * (kc & 3))) & 0x7fu;
+                return w_s + kc * kClusterBr + ((sk & 15u) + 1u) * kGrpB + (sk >> 4) * 16u;
+            };
+            const uint32_t nk = 8u - nslot;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) ra[kk] = next_row();
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) xr[t][u] = 0u;
+                if (work && t < (int)nslot) {
+                    const uint32_t ct = (slots >> (4 * t)) & 15u;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) xr[t][u] = rmask[u];
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        uint32_t r[4];
+                        lds4(ra[kk] + (ct << 7), r);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) xr[t][u] &= r[u];
+                    }
+                }
+            }
+            if (work && nk > 4) {
+#pragma unroll
+                for (int kk = 4; kk < 8; ++kk) ra[kk] = next_row();
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (t < (int)nslot) {
+                        const uint32_t ct = (slots >> (4 * t)) & 15u;
+#pragma unroll
+                        for (int kk = 4; kk < 8; ++kk) {
+                            if (kk < (int)nk) {
+                                uint32_t r[4];
+                                lds4(ra[kk] + (ct << 7), r);
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) xr[t][u] &= r[u];
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        // ---- a6 synchronous rounds on the erased clusters (known clusters frozen)
+        int it = 0;
+        int status = GB_MAX_ITERS;
+        if (!work || nslot == 0) {
+            status = GB_CONVERGED;
+        } else {
+            while (it < T) {
+                uint32_t xn[4][4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) xn[t][u] = xr[t][u];
+#pragma unroll
+                for (int s = 0; s < 4; ++s) {
+                    if (s < (int)nslot) {
+                        const uint32_t sb = w_s + ((slots >> (4 * s)) & 15u) * kClusterBr;
+                        // the source's candidate bits rotated right by 16q: half-word kk of c is
+                        // half-word (kk + q) & 7 of the source
+                        uint32_t c[4];
+                        {
+                            uint32_t a[4], b[4];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) a[j] = rot1 ? xr[s][(j + 1) & 3] : xr[s][j];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) b[j] = rot2 ? a[(j + 2) & 3] : a[j];
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) c[j] = __funnelshift_r(b[j], b[(j + 1) & 3], rots);
+                        }
+                        uint32_t off[NR];   // lowest candidate of each half-word (group 0 if none)
+#pragma unroll
+                        for (int kk = 0; kk < NR; ++kk) {
+                            const uint32_t hw = (kk & 1) ? (c[kk >> 1] >> 16) : (c[kk >> 1] & 0xffffu);
+                            off[kk] = qk(kk) + (uint32_t)__ffs(hw) * kGrpB;
+                        }
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            if (t != s && t < (int)nslot) {
+                                const uint32_t pbase = sb + (((slots >> (4 * t)) & 15u) << 7);
+                                uint32_t r[NR][4];
+#pragma unroll
+                                for (int kk = 0; kk < NR; ++kk) lds4(pbase + off[kk], r[kk]);
+                                uint32_t h[4], miss = 0u;
+#pragma unroll
+                                for (int v = 0; v < 4; ++v) {
+                                    h[v] = r[0][v];
+#pragma unroll
+                                    for (int kk = 1; kk < NR; ++kk) h[v] |= r[kk][v];
+                                    miss |= xn[t][v] & ~h[v];
+                                }
+                                if (miss) {
+                                    // the source's other candidates, a step at a time: each step reads the
+                                    // next candidate of every half-word (8 loads in flight, still one bank
+                                    // group per lane of a quarter-warp) until covered or exhausted
+                                    uint32_t hw[8];
+#pragma unroll
+                                    for (int kk = 0; kk < 8; ++kk) {
+                                        uint32_t x = (kk & 1) ? (c[kk >> 1] >> 16) : (c[kk >> 1] & 0xffffu);
+                                        if (kk < NR) x &= x - 1u;
+                                        hw[kk] = x;
+                                    }
+                                    while (miss && (((hw[0] | hw[1]) | (hw[2] | hw[3])) | ((hw[4] | hw[5]) | (hw[6] | hw[7])))) {
+#pragma unroll
+                                        for (int g = 0; g < 2; ++g) {   // two groups of 4 (registers)
+                                            uint32_t rr[4][4];
+#pragma unroll
+                                            for (int kk = 0; kk < 4; ++kk) {
+                                                lds4(pbase + qk(4 * g + kk) + (uint32_t)__ffs(hw[4 * g + kk]) * kGrpB, rr[kk]);
+                                                hw[4 * g + kk] &= hw[4 * g + kk] - 1u;
+                                            }
+#pragma unroll
+                                            for (int v = 0; v < 4; ++v) h[v] |= (rr[0][v] | rr[1][v]) | (rr[2][v] | rr[3][v]);
+                                        }
+                                        miss = 0u;
+#pragma unroll
+                                        for (int v = 0; v < 4; ++v) {
+                                            miss |= xn[t][v] & ~h[v];
+                                        }
+                                    }
+#pragma unroll
+                                    for (int v = 0; v < 4; ++v) xn[t][v] &= h[v];
+                                }
+                            }
+                        }
+                    }
+                }
+                bool changed = false;
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        changed |= (xr[t][u] != xn[t][u]);
+                        xr[t][u] = xn[t][u];
+                    }
+                }
+                ++it;
+                if (!changed) {
+                    status = GB_CONVERGED;
+                    break;
+                }
+            }
+        }
+        // ---- a7 output
+        if (live) {
+            out_iters[p] = (uint16_t)it;
+            out_status[p] = (uint8_t)(bad ? GB_INVALID : status);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        if (live) {
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                if (bad || !((emask >> c) & 1u)) {
+                    const uint32_t s = bad ? 0xffffffffu : sym(c);
+                    const uint32_t b = 1u << (s & 31u), w = s >> 5;
+                    sts4(my_row + (((uint32_t)c ^ sw) << 4), w == 0 ? b : 0u, w == 1 ? b : 0u, w == 2 ? b : 0u,
+                         w == 3 ? b : 0u);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (!bad && t < (int)nslot) {
+                    const uint32_t c = (slots >> (4 * t)) & 15u;
+                    sts4(my_row + ((c ^ sw) << 4), xr[t][0], xr[t][1], xr[t][2], xr[t][3]);
+                }
+            }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile(
+                "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                ::"l"((uint64_t)&omap), "r"(0), "r"((int)pb), "r"(stg) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 }  // namespace
 
 bool decode_hyb8_supported(const gb_net *net, int rule, int64_t k, const void *state) {
@@ -448,22 +640,46 @@ static bool encode_out_map(void *state, int64_t k, CUtensorMap *map) {
 
 // Narrow (e <= 4) pass of the C = 8 hybrid decode; probes with e > 4 are appended
 // to `ovf` for decode_smem_kernel's list mode (launched by the caller).
+// Rows of the dense kernel's first push step: the fewest (5..8) for which a target's expected
+// candidates n_t = 1 + (L - 1) d^4 (e = 4, four known rows) are all covered by n
+// random candidate rows except with probability n_t (1 - d)^n <= 0.007 -- the rate at which the
+// further steps cost less than the rows saved (same-box A/B, c=8 l=128, 10^7 probes: d = 0.70
+// (C3) 7 rows 0.781 ms vs 8: 0.802, 6: 0.900; d = 0.78 6 rows 0.717 vs 7: 0.735; d = 0.84 6 rows
+// 0.695 vs 7: 0.733).
+static int hyb8_rows(double d, int L) {
+    const double nt = 1.0 + (L - 1) * d * d * d * d;
+    double miss = nt;
+    for (int n = 1; n <= 8; ++n) {
+        miss *= 1.0 - d;
+        if (n >= 5 && miss <= 0.007) return n;
+    }
+    return 8;
+}
+
 cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                                uint16_t *iters, uint8_t *status, int64_t *ovf, unsigned long long *ovf_count) {
     const gb_net *net = cl.net;
     // the output tensor map is a kernel parameter (copied at launch): encoded per call
     alignas(64) CUtensorMap map;
     if (!encode_out_map(state, k, &map)) return cudaErrorNotSupported;
-    // push variant by W's density (see the kernel's comment); GB_OPT_HYB8_SPLIT forces it
+    // kernel by W's density (see the kernels' comments); GB_OPT_HYB8_SPLIT forces it
     const int fs = cl.opt(kOptHyb8Split);
-    const bool dense = fs >= 0 ? (fs != 0) : (net->density.load(std::memory_order_relaxed) > 0.65);
-    auto fn = dense ? decode_hyb8_kernel<true> : decode_hyb8_kernel<false>;   // compile-time variants
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    const double d = net->density.load(std::memory_order_relaxed);
+    const bool dense = fs >= 0 ? (fs != 0) : (d > 0.65);
+    int nr = cl.opt(kOptHyb8Rows);
+    if (nr == 0) nr = hyb8_rows(d, net->s.L);
+    auto fn = !dense ? decode_hyb8_kernel
+              : nr == 5 ? decode_hyb8r_kernel<5>
+              : nr == 6 ? decode_hyb8r_kernel<6>
+              : nr == 7 ? decode_hyb8r_kernel<7> : decode_hyb8r_kernel<8>;
+    const int nt = dense ? kNTr : kNT;
+    const size_t smem = dense ? kSmemR : kSmem;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    int64_t grid = (k + kNT - 1) / kNT;
+    int64_t grid = (k + nt - 1) / nt;
     if (grid > net->sm_count) grid = net->sm_count;
-    fn<<<(unsigned)grid, kNT, kSmem, cl.st>>>(net->wb, probes, k, net->s.L, max_iters, map, iters, status, ovf,
-                                              ovf_count);
+    fn<<<(unsigned)grid, nt, smem, cl.st>>>(net->wb, probes, k, net->s.L, max_iters, map, iters, status, ovf,
+                                             ovf_count);
     cl.launched();
     return cudaGetLastError();
 }

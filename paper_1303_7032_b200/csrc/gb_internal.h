@@ -153,8 +153,9 @@ enum : int {
     kOptSomTensor = 2,     // exact sum-of-max on the tensor cores (N2)
     kOptHyb8 = 3,          // C = 8 hybrid kernel
     kOptL2t = 4,           // thread-per-probe L2 bit kernel
-    kOptHyb8Split = 5,     // push variant of the C = 8 hybrid kernel: -1 by density, 0 loop, 1 staged
+    kOptHyb8Split = 5,     // C = 8 hybrid kernel: -1 by density, 0 sparse loop, 1 dense rotated layout
     kOptStoreScatter = 6,  // store with scattered byte writes only (no privatised tiles)
+    kOptHyb8Rows = 7,      // rows of the dense C = 8 hybrid kernel's first push step: 0 by density, 5..8
 };
 int option_default(int o);
 

@@ -169,9 +169,13 @@ def test_options_api(gb):
     assert net.option("sos_pair") == 1 and net.option("hyb8_split") == -1 and net.option("som_tensor") == 0
     net.set_option("hyb8", 0)
     assert net.decode_kernel(2) == "decode_smem_kernel"
-    for bad in ((99, 1), (0, 2), (0, -1), (5, -2)):
+    for bad in ((99, 1), (0, 2), (0, -1), (5, -2), (7, 1), (7, 4), (7, 9), (7, -1)):
         with pytest.raises(gb.GBError):
             net.set_option(*bad)
+    assert net.option("hyb8_rows") == 0
+    for nr in (5, 6, 7, 8, 0):
+        net.set_option("hyb8_rows", nr)
+        assert net.option("hyb8_rows") == nr
     net.close()
 
 
