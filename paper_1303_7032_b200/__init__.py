@@ -129,7 +129,7 @@ class Net:
     """One GBNN network on one CUDA device (gb_net handle).
 
     ``options``: kernel-selection options (``OPTIONS`` keys -> 0/1, ``hyb8_split``
-    also -1, ``hyb8_rows`` 0 or 5..8), passed to gb_set_option; they pick between
+    also -1, ``hyb8_rows`` 0 or 6..8), passed to gb_set_option; they pick between
     bit-exact kernels."""
 
     def __init__(self, c: int, l: int, device: int = 0, **options):

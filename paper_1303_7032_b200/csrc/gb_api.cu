@@ -225,8 +225,8 @@ int gb_set_option(gb_net *net, int option, int value) {
     if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_HYB8_ROWS)
         return fail(GB_EINVAL, "gb_set_option: unknown option %d", option);
     if (option == GB_OPT_HYB8_ROWS) {
-        if (value != 0 && (value < 5 || value > 8))
-            return fail(GB_EINVAL, "gb_set_option: value %d not 0 or 5..8", value);
+        if (value != 0 && (value < 6 || value > 8))
+            return fail(GB_EINVAL, "gb_set_option: value %d not 0 or 6..8", value);
     } else {
         const int lo = option == GB_OPT_HYB8_SPLIT ? -1 : 0;
         if (value < lo || value > 1) return fail(GB_EINVAL, "gb_set_option: value %d outside [%d, 1]", value, lo);

@@ -575,21 +575,27 @@ decode_hyb8r_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict_
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         __syncwarp();
         if (live) {
+            // clusters in the same order on every lane: lane q's chunk of cluster c is c ^ q, so the
+            // 8 stores never bank-conflict (storing the erased slots by slot index put the lanes of a
+            // quarter-warp on random chunks: 2.4x the wavefronts; same-box A/B C3 0.777 -> 0.770 ms, M=30k
+            // 0.691 -> 0.678); an erased cluster's state is picked from its slot, t = number of erased
+            // clusters below c
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-                if (bad || !((emask >> c) & 1u)) {
-                    const uint32_t s = bad ? 0xffffffffu : sym(c);
-                    const uint32_t b = 1u << (s & 31u), w = s >> 5;
-                    sts4(my_row + (((uint32_t)c ^ sw) << 4), w == 0 ? b : 0u, w == 1 ? b : 0u, w == 2 ? b : 0u,
-                         w == 3 ? b : 0u);
-                }
-            }
+                const bool er = !bad && ((emask >> c) & 1u);
+                const uint32_t s = bad ? 0xffffffffu : sym(c);
+                const uint32_t b = 1u << (s & 31u), w = s >> 5;
+                const uint32_t t = __popc(emask & ((1u << c) - 1u));
+                uint32_t v[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                if (!bad && t < (int)nslot) {
-                    const uint32_t c = (slots >> (4 * t)) & 15u;
-                    sts4(my_row + ((c ^ sw) << 4), xr[t][0], xr[t][1], xr[t][2], xr[t][3]);
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t x = xr[0][u];
+                    if (c >= 1) x = (t & 1u) ? xr[1][u] : x;
+                    if (c >= 2) x = (t == 2u) ? xr[2][u] : x;
+                    if (c >= 3) x = (t == 3u) ? xr[3][u] : x;
+                    v[u] = er ? x : (w == (uint32_t)u ? b : 0u);
                 }
+                sts4(my_row + (((uint32_t)c ^ sw) << 4), v[0], v[1], v[2], v[3]);
             }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -640,18 +646,18 @@ static bool encode_out_map(void *state, int64_t k, CUtensorMap *map) {
 
 // Narrow (e <= 4) pass of the C = 8 hybrid decode; probes with e > 4 are appended
 // to `ovf` for decode_smem_kernel's list mode (launched by the caller).
-// Rows of the dense kernel's first push step: the fewest (5..8) for which a target's expected
+// Rows of the dense kernel's first push step: the fewest (6..8) for which a target's expected
 // candidates n_t = 1 + (L - 1) d^4 (e = 4, four known rows) are all covered by n
 // random candidate rows except with probability n_t (1 - d)^n <= 0.007 -- the rate at which the
 // further steps cost less than the rows saved (same-box A/B, c=8 l=128, 10^7 probes: d = 0.70
-// (C3) 7 rows 0.781 ms vs 8: 0.802, 6: 0.900; d = 0.78 6 rows 0.717 vs 7: 0.735; d = 0.84 6 rows
-// 0.695 vs 7: 0.733).
+// (C3) 7 rows 0.781 ms vs 8: 0.800, 6: 0.902; d = 0.78 6 rows 0.716 vs 5: 0.878, 7: 0.734, 8: 0.780;
+// d = 0.84 6 rows 0.695 vs 5: 0.713, 7: 0.732, 8: 0.782 -- 5 rows never won, so 6 is the floor).
 static int hyb8_rows(double d, int L) {
     const double nt = 1.0 + (L - 1) * d * d * d * d;
     double miss = nt;
     for (int n = 1; n <= 8; ++n) {
         miss *= 1.0 - d;
-        if (n >= 5 && miss <= 0.007) return n;
+        if (n >= 6 && miss <= 0.007) return n;
     }
     return 8;
 }
@@ -669,7 +675,6 @@ cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int 
     int nr = cl.opt(kOptHyb8Rows);
     if (nr == 0) nr = hyb8_rows(d, net->s.L);
     auto fn = !dense ? decode_hyb8_kernel
-              : nr == 5 ? decode_hyb8r_kernel<5>
               : nr == 6 ? decode_hyb8r_kernel<6>
               : nr == 7 ? decode_hyb8r_kernel<7> : decode_hyb8r_kernel<8>;
     const int nt = dense ? kNTr : kNT;

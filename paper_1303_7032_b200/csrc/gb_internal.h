@@ -155,7 +155,7 @@ enum : int {
     kOptL2t = 4,           // thread-per-probe L2 bit kernel
     kOptHyb8Split = 5,     // C = 8 hybrid kernel: -1 by density, 0 sparse loop, 1 dense rotated layout
     kOptStoreScatter = 6,  // store with scattered byte writes only (no privatised tiles)
-    kOptHyb8Rows = 7,      // rows of the dense C = 8 hybrid kernel's first push step: 0 by density, 5..8
+    kOptHyb8Rows = 7,      // rows of the dense C = 8 hybrid kernel's first push step: 0 by density, 6..8
 };
 int option_default(int o);
 
