@@ -552,7 +552,7 @@ def main():
                       "h2d_bytes_per_step": int(my_msgs.nbytes + probes.nbytes),
                       "d2h_bytes_per_step": int(k * (4 * nw + 3)),
                       "how": "gb_store + gb_seal + gb_decode with pinned host buffers (library-staged, "
-                             "double-buffered H2D/kernel/D2H); the full final state bits come back"}
+                             "H2D / kernel / D2H pipelined on three streams); the full final state bits come back"}
         ok = (np.array_equal(out_h[0].numpy(), out[0].cpu().numpy()) and
               np.array_equal(out_h[1].numpy(), out[1].cpu().numpy()))
         state_bits["matches_device_path"] = bool(ok)
@@ -580,7 +580,7 @@ def main():
                "h2d_bytes_per_step": int(my_msgs.nbytes + probes.nbytes),
                "d2h_bytes_per_step": int(k * (2 * c + 3)),
                "how": "gb_store + gb_seal + gb_decode_symbols with pinned host buffers (library-staged, "
-                      "double-buffered H2D/kernel/D2H): the retrieved message per probe (one uint16 per "
+                      "H2D / kernel / D2H pipelined on three streams): the retrieved message per probe (one uint16 per "
                       "cluster) + rounds + status",
                "matches_device_path": bool(np.array_equal(sym_h[1].numpy(), out[1].cpu().numpy()) and
                                            np.array_equal(sym_h[2].numpy(), out[2].cpu().numpy()) and

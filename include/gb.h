@@ -20,8 +20,10 @@
  *  - Every pointer argument is a plain pointer.  For gb_store and gb_decode
  *    buffers may be device pointers (on the handle's device) or host
  *    pointers (pageable or pinned); host buffers are staged through the
- *    library's device scratch and the call then blocks until the results are
- *    back in host memory.  Device-pointer calls are asynchronous and
+ *    library's device scratch (gb_decode*: chunks of 2^19 probes pipelined
+ *    through three slots on a copy-in, a compute and a copy-out stream, so
+ *    both PCIe directions stay busy) and the call then blocks until the
+ *    results are back in host memory.  Device-pointer calls are asynchronous and
  *    stream-ordered on `stream` (a cudaStream_t, NULL = legacy default).
  *  - The caller owns all input/output buffers.  The library owns W (u8 and
  *    bit-packed), its sum-of-sum operands W8 + gamma*I, and a memory pool.
@@ -104,7 +106,7 @@ enum {
                                   large batches                                      */
     GB_OPT_HYB8_ROWS = 7       /* 0 (default): rows of the rotated-layout hybrid
                                   kernel's first push step chosen by W's density;
-                                  5..8 force it (bit-exact either way)               */
+                                  6..8 force it (bit-exact either way)               */
 };
 
 /* gb_decode_ex flags. */
@@ -159,7 +161,7 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
 
 /*
  * gb_set_option / gb_get_option -- per-handle kernel selection (GB_OPT_*).
- * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1; GB_OPT_HYB8_ROWS 0 or 5..8).
+ * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1; GB_OPT_HYB8_ROWS 0 or 6..8).
  * GB_EINVAL for an unknown
  * option or value.  Not to be called while decodes on the handle run.
  */

@@ -176,8 +176,10 @@ int gb_create(int c, int l, int device, gb_net **out) {
     net->wu = net->wb + (size_t)s.np * s.nw;
     net->dflag = reinterpret_cast<unsigned *>(reinterpret_cast<char *>(net->dcount) + 8);
     cudaMemset(net->dcount, 0, 32);
-    for (int i = 0; i < 2; ++i) cudaStreamCreateWithFlags(&net->stage_stream[i], cudaStreamNonBlocking);
+    for (int i = 0; i < 3; ++i) cudaStreamCreateWithFlags(&net->stage_stream[i], cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&net->stage_event, cudaEventDisableTiming);
+    for (auto &sl : net->slot_ev)
+        for (auto &ev : sl) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&net->seal_event, cudaEventDisableTiming);
     // per-call scratch comes from this pool (stream-ordered); keep freed blocks for reuse
     cudaMemPoolProps pp = {};
@@ -203,9 +205,12 @@ int gb_destroy(gb_net *net) {
     if (!net) return GB_OK;
     DeviceGuard g(net->device);
     cudaDeviceSynchronize();
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
         if (net->stage_stream[i]) cudaStreamDestroy(net->stage_stream[i]);
     if (net->stage_event) cudaEventDestroy(net->stage_event);
+    for (auto &sl : net->slot_ev)
+        for (auto &ev : sl)
+            if (ev) cudaEventDestroy(ev);
     if (net->seal_event) cudaEventDestroy(net->seal_event);
     for (auto &v : net->gvar) {
         cudaFree(v.w8g);
@@ -427,58 +432,70 @@ static int decode_impl(gb_net *net, const uint16_t *probes, int64_t k, int rule,
     if (l0 || l1 || l2 || l3)
         return fail(GB_EINVAL, "gb_decode: mix of host and device buffers");
 
-    // Host buffers: double-buffered pipeline over the handle's two staging streams;
-    // chunk i: H2D probes -> decode -> D2H results, overlapping with chunk i+1's copies.
-    // Every chunk is its own call (private scratch).  Ordered after `stream`'s prior work;
-    // blocks until done; host-buffer calls on one handle are serialised.
+    // Host buffers: a three-stage pipeline over the handle's copy-in, compute and copy-out
+    // streams and kStageSlots staging slots: chunk i's H2D copy (slot i % 3, once the copy-out of
+    // chunk i - 3 has left that slot), its decode (after its H2D), its D2H copies (after its
+    // decode).  The two copy directions run concurrently (PCIe is full duplex) instead of
+    // alternating.  Every chunk is its own call (private scratch).  Ordered after `stream`'s
+    // prior work; blocks until done; host-buffer calls on one handle are serialised.
     std::lock_guard<std::mutex> lk(net->stage_mu);
+    constexpr int NS = gb_net::kStageSlots;
     const size_t pin = (size_t)net->s.C * sizeof(uint16_t);
     const size_t pout = (size_t)net->s.nw * sizeof(uint32_t) + sizeof(uint16_t) + sizeof(uint8_t) +
                         (sym ? (size_t)net->s.C * sizeof(uint16_t) : 0);
     const int64_t chunk = std::min<int64_t>(k, 1 << 19);
     const size_t slot = ((size_t)chunk * (pin + pout) + 512 + 255) & ~(size_t)255;
     char *stage = nullptr;
-    GB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&stage), 2 * slot, net->pool, st),
+    GB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&stage), NS * slot, net->pool, st),
             "gb_decode: staging buffer");
     GB_CUDA(cudaEventRecord(net->stage_event, st), "gb_decode: record");
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
         GB_CUDA(cudaStreamWaitEvent(net->stage_stream[i], net->stage_event, 0), "gb_decode: wait");
+    cudaStream_t s_in = net->stage_stream[0], s_k = net->stage_stream[1], s_out = net->stage_stream[2];
     int64_t ci = 0;
     int rc = GB_OK;
     for (int64_t s0 = 0; s0 < k && rc == GB_OK; s0 += chunk, ++ci) {
         const int64_t n = std::min(chunk, k - s0);
-        const int sl = (int)(ci & 1);
-        cudaStream_t ss = net->stage_stream[sl];
+        const int sl = (int)(ci % NS);
+        cudaEvent_t *ev = net->slot_ev[sl];   // [0] copied in, [1] decoded, [2] copied out
         char *base = stage + sl * slot;
         uint16_t *dp = (uint16_t *)base;
         uint32_t *ds = (uint32_t *)(base + (((size_t)chunk * pin + 255) & ~(size_t)255));
         uint16_t *di = (uint16_t *)((char *)ds + (size_t)chunk * net->s.nw * sizeof(uint32_t));
         uint8_t *dt = (uint8_t *)(di + chunk);
         uint16_t *dy = (uint16_t *)(((uintptr_t)(dt + chunk) + 15) & ~(uintptr_t)15);   // symbols
-        cudaError_t e = cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, ss);
+        cudaError_t e = cudaSuccess;
+        if (ci >= NS) e = cudaStreamWaitEvent(s_in, ev[2], 0);   // the slot's previous chunk has left
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dp, probes + s0 * net->s.C, (size_t)n * pin, cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[0], s_in);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_k, ev[0], 0);
         if (e == cudaSuccess) {
-            gb::Call cl(net, ss);
+            gb::Call cl(net, s_k);
             e = gb::launch_decode(cl, dp, n, rule, gamma, max_iters, cyc, ds, di, dt);
         }
         if (e == cudaSuccess && sym) {
-            gb::Call cl(net, ss);
+            gb::Call cl(net, s_k);
             e = gb::launch_symbols(cl, ds, n, dy);
         }
+        if (e == cudaSuccess) e = cudaEventRecord(ev[1], s_k);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s_out, ev[1], 0);
         if (e == cudaSuccess)
             e = sym ? cudaMemcpyAsync(out_sym + s0 * net->s.C, dy, (size_t)n * net->s.C * sizeof(uint16_t),
-                                      cudaMemcpyDeviceToHost, ss)
+                                      cudaMemcpyDeviceToHost, s_out)
                     : cudaMemcpyAsync(out_state + s0 * net->s.nw, ds, (size_t)n * net->s.nw * sizeof(uint32_t),
-                                      cudaMemcpyDeviceToHost, ss);
+                                      cudaMemcpyDeviceToHost, s_out);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, ss);
-        if (e == cudaSuccess) e = cudaMemcpyAsync(out_status + s0, dt, (size_t)n, cudaMemcpyDeviceToHost, ss);
+            e = cudaMemcpyAsync(out_iters + s0, di, (size_t)n * sizeof(uint16_t), cudaMemcpyDeviceToHost, s_out);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(out_status + s0, dt, (size_t)n, cudaMemcpyDeviceToHost, s_out);
+        if (e == cudaSuccess) e = cudaEventRecord(ev[2], s_out);
         if (e != cudaSuccess) rc = cuda_fail(e, "gb_decode: staged chunk");
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < 3; ++i) {
         cudaError_t e = cudaStreamSynchronize(net->stage_stream[i]);
         if (e != cudaSuccess && rc == GB_OK) rc = cuda_fail(e, "gb_decode: sync");
     }
-    cudaFreeAsync(stage, st);   // both staging streams are idle now
+    cudaFreeAsync(stage, st);   // the staging streams are idle now
     return rc;
 }
 

@@ -97,8 +97,12 @@ struct gb_net {
     cudaMemPool_t pool = nullptr;
     // host-buffer staging (gb_decode / gb_store with host pointers): serialised per handle
     std::mutex stage_mu;
-    cudaStream_t stage_stream[2] = {nullptr, nullptr};
+    // host-buffer decode pipeline: [0] copy-in, [1] compute, [2] copy-out streams; per staging
+    // slot the events "copied in", "decoded", "copied out"
+    static constexpr int kStageSlots = 3;
+    cudaStream_t stage_stream[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t stage_event = nullptr;
+    cudaEvent_t slot_ev[kStageSlots][3] = {};
     std::atomic<long long> launches{0};      // kernels launched by this handle (diagnostics)
     alignas(64) unsigned char wmap[128];     // CUtensorMap of W8 for the 4-warp SOS kernel
     bool wmap_ok = false;

@@ -99,13 +99,14 @@ def test_concurrent_decodes_one_handle(gb):
 @pytest.mark.parametrize("c,l,m,rule,e", [(8, 128, 5000, 0, 4), (8, 128, 5000, 1, 4), (8, 128, 20000, 2, -1),
                                           (16, 256, 20000, 2, 8)])
 def test_host_buffers_multichunk_all_kernels(gb, c, l, m, rule, e):
-    """Host (pinned) buffers with k > 2^19: the library stages chunks on two
-    streams, each chunk a call with its own scratch (work queue, overflow
-    list, L2 state scratch).  Results equal the device-pointer decode for the
+    """Host (pinned) buffers with k = 4 * 2^19 + 4321: the library pipelines 5
+    chunks of 2^19 through 3 staging slots (copy-in, compute and copy-out
+    streams; slots reused), each chunk a call with its own scratch (work queue,
+    overflow list, L2 state scratch).  Results equal the device-pointer decode for the
     pair SOS kernel, the SOM shared-memory kernel, the C=8 hybrid kernel with
     mixed erasure counts (list mode) and the L2 thread-per-probe kernel; a
     sample equals the oracle."""
-    k = (1 << 19) + 4321
+    k = (1 << 21) + 4321
     msgs = gbgen.messages(51 + c, m, c, l)
     ee = np.random.default_rng(3).integers(0, c + 1, size=k) if e < 0 else e
     pr, _ = gbgen.probes(52 + c, msgs, k, ee, l, random_count=k // 20)
@@ -169,11 +170,11 @@ def test_options_api(gb):
     assert net.option("sos_pair") == 1 and net.option("hyb8_split") == -1 and net.option("som_tensor") == 0
     net.set_option("hyb8", 0)
     assert net.decode_kernel(2) == "decode_smem_kernel"
-    for bad in ((99, 1), (0, 2), (0, -1), (5, -2), (7, 1), (7, 4), (7, 9), (7, -1)):
+    for bad in ((99, 1), (0, 2), (0, -1), (5, -2), (7, 1), (7, 5), (7, 9), (7, -1)):
         with pytest.raises(gb.GBError):
             net.set_option(*bad)
     assert net.option("hyb8_rows") == 0
-    for nr in (5, 6, 7, 8, 0):
+    for nr in (6, 7, 8, 0):
         net.set_option("hyb8_rows", nr)
         assert net.option("hyb8_rows") == nr
     net.close()
@@ -250,10 +251,10 @@ def test_decode_symbols_matches_oracle(gb, c, l, m, e, k):
 
 
 def test_decode_symbols_host_buffers_chunked(gb):
-    """gb_decode_symbols with host buffers: 2^19 + 4321 probes (two staged chunks on the two
-    staging streams) equal the device-buffer call and gb_decode's states mapped by
+    """gb_decode_symbols with host buffers: 4 * 2^19 + 4321 probes (five staged chunks through
+    three staging slots) equal the device-buffer call and gb_decode's states mapped by
     oracle.symbols; hybrid (C=8 kernel) and sum-of-sum (CTA pair)."""
-    c, l, m, k = 8, 128, 5000, (1 << 19) + 4321
+    c, l, m, k = 8, 128, 5000, (1 << 21) + 4321
     msgs = gbgen.messages(77, m, c, l)
     pr, _ = gbgen.probes(78, msgs, k, 4, l)
     net = gb.Net(c, l)
