@@ -479,7 +479,7 @@ def main():
     hbm, bf16, peak_kind = measured_peaks()
     bytes_per_probe = 2 * c + 4 * nw + 2 + 1
     kernel = net.decode_kernel(rule)
-    if kernel.startswith("sos_"):
+    if kernel.startswith("sos_") and kernel != "sos_bits_kernel":
         # tensor-bound.  Algorithmic int8 ops = sum over probes of its rounds x 2 n_p^2 (Eq.(11) per
         # probe-round).  Both SOS kernels refill converged slots of their 128-probe tiles, so the
         # executed work is the algorithmic work plus the last partial rounds (a fixed-tile kernel
@@ -511,6 +511,16 @@ def main():
                 "algorithmic_bytes_per_probe": bytes_per_probe,
                 "peak_source": peak_kind + " (MEASURED_PEAKS.json hbm_gbs)",
                 "decode_ms_per_launch": dec_ms, "decode_share_of_step": dec_ms / (ms / args.steps)}
+        if kernel == "sos_bits_kernel":
+            # sum-of-sum on the CUDA cores (sparse states): an I/O roofline like the bit kernels; for
+            # comparison, the dense int8 contraction the tensor-core kernels would run for the same
+            # probe-rounds (2 n_p^2 per probe-round) per second of this kernel
+            it_h = out[1].cpu().numpy().view(np.uint16).astype(np.int64)
+            npad = net.n_padded
+            roof["int8_equivalent"] = {"tops": float(it_h.sum()) * 2 * npad * npad / (dec_ms / 1e3) / 1e12,
+                                       "int8_peak_tops": 2.0 * bf16, "probe_rounds": int(it_h.sum()),
+                                       "note": "dense-contraction ops the tensor-core path executes for the "
+                                               "same rounds; this kernel adds only the active rows"}
         wpp = ncu_entry(kernel, args.config).get("smem_wavefronts_per_probe")
         if wpp:
             # the binding on-chip resource of the bit kernels: shared-memory wavefronts through the

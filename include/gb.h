@@ -104,9 +104,13 @@ enum {
     GB_OPT_STORE_SCATTER = 6,  /* 1: gb_store with scattered byte writes only;
                                   0 (default): shared-memory privatised tiles for
                                   large batches                                      */
-    GB_OPT_HYB8_ROWS = 7       /* 0 (default): rows of the rotated-layout hybrid
+    GB_OPT_HYB8_ROWS = 7,      /* 0 (default): rows of the rotated-layout hybrid
                                   kernel's first push step chosen by W's density;
                                   6..8 force it (bit-exact either way)               */
+    GB_OPT_SOS_BITS = 8        /* -1 (default): sum-of-sum on the CUDA cores (active
+                                  rows into bit-sliced counters) when W is sparse
+                                  (C <= 8, n_padded <= 1024, no cycle exit), else on
+                                  the tensor cores; 0 / 1 force it (bit-exact)       */
 };
 
 /* gb_decode_ex flags. */
@@ -161,7 +165,8 @@ int gb_store(gb_net *net, const uint16_t *msgs, int64_t m, void *stream);
 
 /*
  * gb_set_option / gb_get_option -- per-handle kernel selection (GB_OPT_*).
- * value is 0 or 1 (GB_OPT_HYB8_SPLIT also -1; GB_OPT_HYB8_ROWS 0 or 6..8).
+ * value is 0 or 1 (GB_OPT_HYB8_SPLIT and GB_OPT_SOS_BITS also -1;
+ * GB_OPT_HYB8_ROWS 0 or 6..8).
  * GB_EINVAL for an unknown
  * option or value.  Not to be called while decodes on the handle run.
  */

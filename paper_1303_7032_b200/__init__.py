@@ -37,7 +37,8 @@ EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_set_option", "
 
 # gb_set_option keys (include/gb.h GB_OPT_*): kernel choices with identical results
 OPTIONS = {"sos_pair": 0, "sos_streamed": 1, "som_tensor": 2, "hyb8": 3, "l2t": 4, "hyb8_split": 5,
-           "store_scatter": 6, "hyb8_rows": 7}
+           "store_scatter": 6, "hyb8_rows": 7,
+           "sos_bits": 8}
 
 _lib = None
 

@@ -227,13 +227,13 @@ int gb_destroy(gb_net *net) {
 
 int gb_set_option(gb_net *net, int option, int value) {
     if (!net) return fail(GB_EINVAL, "gb_set_option: net is NULL");
-    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_HYB8_ROWS)
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_SOS_BITS)
         return fail(GB_EINVAL, "gb_set_option: unknown option %d", option);
     if (option == GB_OPT_HYB8_ROWS) {
         if (value != 0 && (value < 6 || value > 8))
             return fail(GB_EINVAL, "gb_set_option: value %d not 0 or 6..8", value);
     } else {
-        const int lo = option == GB_OPT_HYB8_SPLIT ? -1 : 0;
+        const int lo = (option == GB_OPT_HYB8_SPLIT || option == GB_OPT_SOS_BITS) ? -1 : 0;
         if (value < lo || value > 1) return fail(GB_EINVAL, "gb_set_option: value %d outside [%d, 1]", value, lo);
     }
     net->opt[option].store(value);
@@ -242,7 +242,7 @@ int gb_set_option(gb_net *net, int option, int value) {
 
 int gb_get_option(gb_net *net, int option, int *value) {
     if (!net || !value) return fail(GB_EINVAL, "gb_get_option: NULL argument");
-    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_HYB8_ROWS)
+    if (option < 0 || option >= gb::kNumOptions || option > GB_OPT_SOS_BITS)
         return fail(GB_EINVAL, "gb_get_option: unknown option %d", option);
     *value = net->opt[option].load();
     return GB_OK;
@@ -525,13 +525,15 @@ int gb_info(gb_net *net, int *c, int *l, int *n_padded, int64_t *stored_count) {
 
 const char *gb_decode_kernel(gb_net *net, int rule) {
     if (!net) return "";
+    if (rule == GB_SUM_OF_SUM && gb::sos_bits_chosen(net, 0, 0)) return "sos_bits_kernel";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc3_enabled(net))
         return gb::sos_tc3_pair(net) ? "sos_tc3x2_kernel" : "sos_tc3_kernel";
     if (rule == GB_SUM_OF_SUM && gb::sos_tc2_supported(net->s))
         return gb::sos_2cta_enabled(net) ? "sos_tc2x2_kernel" : "sos_tc2_kernel";
     if (rule == GB_SUM_OF_SUM && net->wmap_ok && gb::sos_tc_supported(net->s)) return "sos_tc_kernel";
     if (rule == GB_SUM_OF_MAX && gb::som_tc_enabled(net)) return "som_tc_kernel";
-    if (rule == GB_HYBRID && gb::decode_hyb8_supported(net, rule, 0, nullptr)) return "decode_hyb8_kernel";
+    if (rule == GB_HYBRID && gb::decode_hyb8_supported(net, rule, 0, nullptr))
+        return gb::decode_hyb8_rotated(net) ? "decode_hyb8r_kernel" : "decode_hyb8_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_smem_supported(net->s, rule)) return "decode_smem_kernel";
     if (rule != GB_SUM_OF_SUM && gb::decode_l2_supported(net->s, rule))
         return gb::decode_l2t_supported(net, rule) ? "decode_l2t_kernel" : "decode_l2_kernel";
@@ -557,6 +559,7 @@ int option_default(int o) {
         case kOptL2t: return 1;
         case kOptHyb8Split: return -1;
         case kOptStoreScatter: return 0;
+        case kOptSosBits: return -1;
         default: return 0;
     }
 }
@@ -583,9 +586,9 @@ void *Call::alloc(size_t bytes) {
 
 unsigned long long *Call::counters() {
     if (!counters_) {
-        counters_ = alloc_n<unsigned long long>(2);
+        counters_ = alloc_n<unsigned long long>(3);
         if (!counters_) return nullptr;
-        cudaError_t e = cudaMemsetAsync(counters_, 0, 2 * sizeof(unsigned long long), st);
+        cudaError_t e = cudaMemsetAsync(counters_, 0, 3 * sizeof(unsigned long long), st);
         if (e != cudaSuccess) {
             err = e;
             counters_ = nullptr;
@@ -599,13 +602,28 @@ int64_t *Call::ovf(int64_t k) {
     return ovf_;
 }
 
+// W density below which sum-of-sum runs on the CUDA cores (gb_decode_sos_bits.cu).  Measured
+// crossover (c=8 l=128 e=4, 10^6 probes, sos_bits vs sos_tc2x2 ms): M=3k (d=0.17) 0.60 vs 1.92,
+// M=5k (0.26) 1.35 vs 2.51, M=6.5k (0.33) 1.76 vs 2.97, M=8k (0.39) 2.87 vs 3.45, M=10k (0.46)
+// 4.45 vs 3.81.
+constexpr double kSosBitsDensity = 0.4;
+
+bool sos_bits_chosen(const gb_net *net, int gamma, int cyc) {
+    const int ob = net->opt[kOptSosBits].load(std::memory_order_relaxed);
+    return sos_bits_supported(net->s, gamma, cyc) &&
+           (ob == 1 || (ob < 0 && net->density.load(std::memory_order_relaxed) < kSosBitsDensity));
+}
+
 // Kernel selection for one decode call.
 cudaError_t launch_decode(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma, int max_iters, int cyc,
                           uint32_t *state, uint16_t *iters, uint8_t *status) {
     gb_net *net = cl.net;
     cudaError_t e = cudaErrorNotSupported;
     if (rule == GB_SUM_OF_SUM) {
-        if (sos_tc2_supported(net->s) || sos_tc3_enabled(net) || (net->wmap_ok && sos_tc_supported(net->s)))
+        // sparse states (low W density): active rows into bit-sliced counters on the CUDA cores
+        if (sos_bits_chosen(net, gamma, cyc))
+            e = launch_sos_bits(cl, probes, k, gamma, max_iters, state, iters, status);
+        else if (sos_tc2_supported(net->s) || sos_tc3_enabled(net) || (net->wmap_ok && sos_tc_supported(net->s)))
             e = launch_decode_sos_tc(cl, probes, k, gamma, max_iters, cyc, state, iters, status);
     } else {
         if (rule == GB_SUM_OF_MAX && som_tc_enabled(net))

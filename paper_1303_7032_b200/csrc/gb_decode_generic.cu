@@ -38,7 +38,8 @@ __device__ __forceinline__ unsigned real_mask(const Shape &s, int u) {
 __global__ void __launch_bounds__(kWarps * 32)
 decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__restrict__ probes,
                       int64_t k, int rule, int gamma, int T, int cyc_exit, uint32_t *__restrict__ out_state,
-                      uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status) {
+                      uint16_t *__restrict__ out_iters, uint8_t *__restrict__ out_status,
+                      const int64_t *__restrict__ list, const unsigned long long *__restrict__ list_count) {
     extern __shared__ uint32_t smem[];
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -47,7 +48,10 @@ decode_generic_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *
     uint32_t *bufB = bufA + nw;
     int *wmax = reinterpret_cast<int *>(bufB + nw);
 
-    for (int64_t p = (int64_t)blockIdx.x * kWarps + warp; p < k; p += (int64_t)gridDim.x * kWarps) {
+    // list mode: decode the list_count probes whose indices another kernel queued in list
+    const int64_t n = list ? (int64_t)*list_count : k;
+    for (int64_t i = (int64_t)blockIdx.x * kWarps + warp; i < n; i += (int64_t)gridDim.x * kWarps) {
+        const int64_t p = list ? list[i] : i;
         const uint16_t *pr = probes + p * s.C;
         unsigned long long em = 0ull;
         bool bad = false;
@@ -201,7 +205,25 @@ cudaError_t launch_decode_generic(Call &cl, const uint16_t *probes, int64_t k, i
         if (e != cudaSuccess) return e;
     }
     decode_generic_kernel<<<(unsigned)grid, kWarps * 32, smem, st>>>(
-        net->s, net->wb, probes, k, rule, gamma, max_iters, cyc, state, iters, status);
+        net->s, net->wb, probes, k, rule, gamma, max_iters, cyc, state, iters, status, nullptr, nullptr);
+    cl.launched();
+    return cudaGetLastError();
+}
+
+// List mode: the *count probes listed in `list` (indices into probes / the outputs), queued by a
+// preceding kernel on the same stream; k bounds the count.
+cudaError_t launch_decode_generic_list(Call &cl, const uint16_t *probes, int64_t k, const int64_t *list,
+                                       const unsigned long long *count, int rule, int gamma, int max_iters,
+                                       uint32_t *state, uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    const size_t smem = (size_t)kWarps * 3 * net->s.nw * sizeof(uint32_t);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(decode_generic_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    decode_generic_kernel<<<(unsigned)net->sm_count, kWarps * 32, smem, cl.st>>>(
+        net->s, net->wb, probes, k, rule, gamma, max_iters, 0, state, iters, status, list, count);
     cl.launched();
     return cudaGetLastError();
 }

@@ -612,6 +612,13 @@ decode_hyb8r_kernel(const uint32_t *__restrict__ wb, const uint16_t *__restrict_
 
 }  // namespace
 
+// The rotated-layout kernel for dense W (density > 0.65, counted by seal), the loop kernel for
+// sparse W; GB_OPT_HYB8_SPLIT forces either.
+bool decode_hyb8_rotated(const gb_net *net) {
+    const int fs = net->opt[kOptHyb8Split].load(std::memory_order_relaxed);
+    return fs >= 0 ? (fs != 0) : (net->density.load(std::memory_order_relaxed) > 0.65);
+}
+
 bool decode_hyb8_supported(const gb_net *net, int rule, int64_t k, const void *state) {
     const Shape &s = net->s;
     return rule == GB_HYBRID && s.C == 8 && s.Wc == 4 && k < (1ll << 31) && ((uintptr_t)state & 15u) == 0 &&
@@ -669,9 +676,8 @@ cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int 
     alignas(64) CUtensorMap map;
     if (!encode_out_map(state, k, &map)) return cudaErrorNotSupported;
     // kernel by W's density (see the kernels' comments); GB_OPT_HYB8_SPLIT forces it
-    const int fs = cl.opt(kOptHyb8Split);
     const double d = net->density.load(std::memory_order_relaxed);
-    const bool dense = fs >= 0 ? (fs != 0) : (d > 0.65);
+    const bool dense = decode_hyb8_rotated(net);
     int nr = cl.opt(kOptHyb8Rows);
     if (nr == 0) nr = hyb8_rows(d, net->s.L);
     auto fn = !dense ? decode_hyb8_kernel

@@ -50,7 +50,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
 sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params P,
                  const uint16_t *__restrict__ probes, int64_t k, int T, unsigned long long *queue,
                  uint32_t *__restrict__ out_state, uint16_t *__restrict__ out_iters,
-                 uint8_t *__restrict__ out_status) {
+                 uint8_t *__restrict__ out_status, const int64_t *__restrict__ list,
+                 const unsigned long long *__restrict__ list_count) {
     constexpr int LP = 32 * WC;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -78,6 +79,10 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     const int nw = s.nw, np = s.np;
     const int nkb = (np + kKB - 1) / kKB;
     const int npass = (np + P.NP - 1) / P.NP;
+    auto pass_cols = [&](int pass, int &n0, int &ncols) {   // pass -> (first column, columns)
+        n0 = pass * P.NP;
+        ncols = min(P.NP, np - n0);
+    };
     const bool narrow = P.gamma_epi + np < 0x7FFF;   // scores fit 15 bits (wta_words)
 
     if (tid == 0) {
@@ -103,6 +108,9 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     uint32_t it_p = 0, it_m = 0, pc_m = 0, pc_e = 0;
     uint32_t par = 0, round = 0;
     uint32_t *V = Vs, *Vn = Vs + nw * kTM;
+    // list mode: decode the *list_count probes whose indices a preceding kernel queued in list
+    if (list) k = (int64_t)*list_count;
+    auto pid = [&](int64_t i) { return list ? list[i] : i; };
     int64_t p = -1, pn = -1;
     uint4 qn = make_uint4(0, 0, 0, 0);
     const bool pack = s.C <= 8;
@@ -123,7 +131,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         qready = true;
         if (pack && pn < k) {
             uint32_t w4[4] = {0u, 0u, 0u, 0u};
-            const uint16_t *pr = probes + pn * s.C;
+            const uint16_t *pr = probes + pid(pn) * s.C;
 #pragma unroll
             for (int c = 0; c < 8; ++c)
                 if (c < s.C) w4[c >> 1] |= (uint32_t)__ldg(pr + c) << (16 * (c & 1));
@@ -147,6 +155,7 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             zmask = 0u;
             rl = 0;
             if (p >= k) { active = false; return; }
+            p = pid(p);
             auto sym_of = [&](int c) -> unsigned {
                 if (pack) {
                     const uint32_t w = (c >> 1) == 0 ? q.x : (c >> 1) == 1 ? q.y : (c >> 1) == 2 ? q.z : q.w;
@@ -198,7 +207,9 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
     int pre = 0;   // K blocks of the coming round already issued
     auto load_block = [&](int j) {
         const int pass = j / nkb, kb = j - pass * nkb;
-        const int n0 = pass * P.NP, ncols = min(P.NP, np - n0), half = ncols >> 1;
+        int n0, ncols;
+        pass_cols(pass, n0, ncols);
+        const int half = ncols >> 1;
         const int st = it_p % S;
         mbar_wait(empty_bar(st), ((it_p / S) & 1u) ^ 1u);
         if (leader) mbar_expect_tx(full_bar(st), (uint32_t)ncols * kKB);   // both halves
@@ -302,7 +313,8 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
         } else if (warp == 1) {
             if (lane == 0 && leader) {   // ---- MMA issuer for the pair
                 for (int pass = 0; pass < npass; ++pass, ++pc_m) {
-                    const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                    int n0, ncols;
+                    pass_cols(pass, n0, ncols);
                     const uint32_t buf = pc_m & 1u;
                     mbar_wait(tempty_bar(buf), ((pc_m >> 1) & 1u) ^ 1u);
                     tc_fence_after();
@@ -329,7 +341,8 @@ sos_tc2x2_kernel(Shape s, const __grid_constant__ CUtensorMap wmap, Pair2Params 
             fetch_syms();
             flush();
             for (int pass = 0; pass < npass; ++pass, ++pc_e) {
-                const int n0 = pass * P.NP, ncols = min(P.NP, np - n0);
+                int n0, ncols;
+                pass_cols(pass, n0, ncols);
                 const uint32_t buf = pc_e & 1u;
                 mbar_wait(tfull_bar(buf), (pc_e >> 1) & 1u);
                 tc_fence_after();
@@ -462,7 +475,8 @@ bool plan_pair(const Shape &s, int gamma_epi, Pair2Params &P, size_t &smem) {
 
 template <int WC>
 cudaError_t launch_pair_t(Call &cl, const void *map, const Pair2Params &P, size_t smem, const uint16_t *probes,
-                          int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+                          int64_t k, int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
+                          const int64_t *list, const unsigned long long *list_count) {
     const gb_net *net = cl.net;
     const cudaStream_t st = cl.st;
     auto fn = sos_tc2x2_kernel<WC>;
@@ -491,10 +505,11 @@ cudaError_t launch_pair_t(Call &cl, const void *map, const Pair2Params &P, size_
     }
     const int64_t npairs = (k + 2 * kTM - 1) / (2 * kTM);
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(npairs, max_clusters[WC].load()));
-    unsigned long long *queue = cl.counters();
+    unsigned long long *queue = cl.counters();   // list mode: the second queue ([2])
+    if (queue && list) queue += 2;
     if (!queue) return cl.err;
     fn<<<2 * pairs, 192, smem, st>>>(net->s, *reinterpret_cast<const CUtensorMap *>(map), P, probes, k,
-                                     max_iters, queue, state, iters, status);
+                                     max_iters, queue, state, iters, status, list, list_count);
     cl.launched();
     return cudaGetLastError();
 }
@@ -515,7 +530,8 @@ int sos_2cta_box_rows(const Shape &s) {
 }
 
 cudaError_t launch_sos_2cta(Call &cl, const void *map, int gamma_epi, int cyc, const uint16_t *probes, int64_t k,
-                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status) {
+                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status, const int64_t *list,
+                            const unsigned long long *list_count) {
     const gb_net *net = cl.net;
     Pair2Params P;
     size_t smem;
@@ -524,11 +540,11 @@ cudaError_t launch_sos_2cta(Call &cl, const void *map, int gamma_epi, int cyc, c
     // one CTA per SM: two 512-column TMEM allocations on one SM could deadlock across pairs
     if (smem < 120 * 1024) smem = 120 * 1024;
     switch (net->s.Wc) {
-        case 1: return launch_pair_t<1>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
-        case 2: return launch_pair_t<2>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
-        case 3: return launch_pair_t<3>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
-        case 4: return launch_pair_t<4>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
-        default: return launch_pair_t<8>(cl, map, P, smem, probes, k, max_iters, state, iters, status);
+        case 1: return launch_pair_t<1>(cl, map, P, smem, probes, k, max_iters, state, iters, status, list, list_count);
+        case 2: return launch_pair_t<2>(cl, map, P, smem, probes, k, max_iters, state, iters, status, list, list_count);
+        case 3: return launch_pair_t<3>(cl, map, P, smem, probes, k, max_iters, state, iters, status, list, list_count);
+        case 4: return launch_pair_t<4>(cl, map, P, smem, probes, k, max_iters, state, iters, status, list, list_count);
+        default: return launch_pair_t<8>(cl, map, P, smem, probes, k, max_iters, state, iters, status, list, list_count);
     }
 }
 

@@ -797,6 +797,21 @@ cudaError_t gamma_operand(Call &cl, int gamma, int box_rows, const void **map) {
     return cudaSuccess;
 }
 
+cudaError_t launch_sos_pair_list(Call &cl, const uint16_t *probes, int64_t k, const int64_t *list,
+                                 const unsigned long long *count, int gamma, int max_iters, uint32_t *state,
+                                 uint16_t *iters, uint8_t *status) {
+    const gb_net *net = cl.net;
+    Sos2Params P2;
+    size_t smem2;
+    if (sos_tc3_enabled(net) || !plan2(net->s, gamma, P2, smem2) || !sos_2cta_enabled(net))
+        return cudaErrorNotSupported;
+    const void *map = nullptr;
+    cudaError_t e = gamma_operand(cl, gamma, sos_2cta_box_rows(net->s), &map);
+    if (e != cudaSuccess) return e;
+    return launch_sos_2cta(cl, map, gamma > 255 ? gamma : 0, 0, probes, k, max_iters, state, iters, status, list,
+                           count);
+}
+
 cudaError_t launch_decode_sos_tc(Call &cl, const uint16_t *probes, int64_t k, int gamma, int max_iters,
                                  int cyc, uint32_t *state, uint16_t *iters, uint8_t *status) {
     const gb_net *net = cl.net;

@@ -34,7 +34,7 @@ struct Status {
 };
 
 // Kernel-selection options of a handle (gb_set_option; GB_OPT_* in gb.h).
-constexpr int kNumOptions = 8;
+constexpr int kNumOptions = 9;
 
 // One W8 + gamma*I operand (gamma folded into the int8 diagonal, 0..255).
 constexpr int kGammaVariants = 4;
@@ -136,7 +136,8 @@ struct Call {
     ~Call();
     void *alloc(size_t bytes);     // nullptr on failure (err set)
     template <class T> T *alloc_n(size_t n) { return static_cast<T *>(alloc(n * sizeof(T))); }
-    // [0] work queue of the slot-refill kernels, [1] overflow count; zeroed once per call
+    // [0] work queue of the slot-refill kernels, [1] overflow count, [2] work queue of a list-mode
+    // kernel decoding the overflow; zeroed once per call
     unsigned long long *counters();
     // overflow list of probe indices (k entries) for the two-pass bit kernels
     int64_t *ovf(int64_t k);
@@ -160,6 +161,7 @@ enum : int {
     kOptHyb8Split = 5,     // C = 8 hybrid kernel: -1 by density, 0 sparse loop, 1 dense rotated layout
     kOptStoreScatter = 6,  // store with scattered byte writes only (no privatised tiles)
     kOptHyb8Rows = 7,      // rows of the dense C = 8 hybrid kernel's first push step: 0 by density, 6..8
+    kOptSosBits = 8,       // sum-of-sum on the CUDA cores for sparse states: -1 by density, 0 off, 1 on
 };
 int option_default(int o);
 
@@ -183,6 +185,14 @@ cudaError_t launch_decode_smem(Call &cl, const uint16_t *probes, int64_t k, int 
                                uint32_t *state, uint16_t *iters, uint8_t *status);
 cudaError_t launch_decode_generic(Call &cl, const uint16_t *probes, int64_t k, int rule, int gamma,
                                   int max_iters, int cyc, uint32_t *state, uint16_t *iters, uint8_t *status);
+cudaError_t launch_decode_generic_list(Call &cl, const uint16_t *probes, int64_t k, const int64_t *list,
+                                       const unsigned long long *count, int rule, int gamma, int max_iters,
+                                       uint32_t *state, uint16_t *iters, uint8_t *status);
+// Sum-of-sum on the CUDA cores for sparse states (gb_decode_sos_bits.cu): C <= 8, n_p <= 1024.
+bool sos_bits_supported(const Shape &s, int gamma, int cyc);
+bool sos_bits_chosen(const gb_net *net, int gamma, int cyc);   // option / density (gb_api.cu)
+cudaError_t launch_sos_bits(Call &cl, const uint16_t *probes, int64_t k, int gamma, int max_iters,
+                            uint32_t *state, uint16_t *iters, uint8_t *status);
 bool sos_tc_supported(const Shape &s);
 bool sos_tc2_supported(const Shape &s);
 bool sos_tc_make_map(gb_net *net);
@@ -195,10 +205,17 @@ cudaError_t gamma_operand(Call &cl, int gamma, int box_rows, const void **map);
 bool sos_2cta_enabled(const gb_net *net);
 int sos_2cta_box_rows(const Shape &s);
 cudaError_t launch_sos_2cta(Call &cl, const void *map, int gamma_epi, int cyc, const uint16_t *probes, int64_t k,
-                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status);
+                            int max_iters, uint32_t *state, uint16_t *iters, uint8_t *status,
+                            const int64_t *list = nullptr, const unsigned long long *list_count = nullptr);
+// The CTA-pair SOS kernel in list mode (the *count probes queued in list; k bounds the count);
+// cudaErrorNotSupported when the pair kernel does not take the shape.
+cudaError_t launch_sos_pair_list(Call &cl, const uint16_t *probes, int64_t k, const int64_t *list,
+                                 const unsigned long long *count, int gamma, int max_iters, uint32_t *state,
+                                 uint16_t *iters, uint8_t *status);
 // C = 8, Wc = 4 hybrid decode of the probes with e <= 4 (gb_decode_hyb8.cu); the
 // others are appended to the overflow list `ovf`.
 bool decode_hyb8_supported(const gb_net *net, int rule, int64_t k, const void *state);
+bool decode_hyb8_rotated(const gb_net *net);   // dense W: decode_hyb8r_kernel
 cudaError_t launch_decode_hyb8(Call &cl, const uint16_t *probes, int64_t k, int max_iters, uint32_t *state,
                                uint16_t *iters, uint8_t *status, int64_t *ovf, unsigned long long *ovf_count);
 // Streamed-A sum-of-sum kernel for 1024 < n_p <= 4096 (gb_decode_sos_tc3.cu); `map` is the

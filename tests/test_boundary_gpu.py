@@ -173,7 +173,12 @@ def test_options_api(gb):
     for bad in ((99, 1), (0, 2), (0, -1), (5, -2), (7, 1), (7, 5), (7, 9), (7, -1)):
         with pytest.raises(gb.GBError):
             net.set_option(*bad)
-    assert net.option("hyb8_rows") == 0
+    assert net.option("hyb8_rows") == 0 and net.option("sos_bits") == -1
+    for v in (-1, 0, 1):
+        net.set_option("sos_bits", v)
+        assert net.option("sos_bits") == v
+    with pytest.raises(gb.GBError):
+        net.set_option("sos_bits", 2)
     for nr in (6, 7, 8, 0):
         net.set_option("hyb8_rows", nr)
         assert net.option("hyb8_rows") == nr

@@ -172,7 +172,8 @@ def test_hyb8_matches_oracle_and_generic(gb, l, m, k):
         pr[7, 0] = 0xFFFE
     w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
     net = make_net(gb, msgs, c, l)
-    assert net.decode_kernel(2) == "decode_hyb8_kernel"
+    dens = w.sum() / max(1, c * (c - 1) * l * l)    # edge density between clusters
+    assert net.decode_kernel(2) == ("decode_hyb8r_kernel" if dens > 0.65 else "decode_hyb8_kernel")
     want = oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=20)
     got = gpu_decode(net, pr, 2, 1, 20)
     assert_same(got, want, 2, f"hyb8 l={l} m={m} k={k}")
@@ -184,6 +185,7 @@ def test_hyb8_matches_oracle_and_generic(gb, l, m, k):
     assert_same(gpu_decode(net, pr, 2, 1, 3), oracle.decode(w, c, l, pr, 2, gamma=1, max_iters=3), 2, "hyb8 T=3")
     for split in (0, 1):                            # sparse loop / rotated layout (density heuristic forced)
         net.set_option("hyb8_split", split)
+        assert net.decode_kernel(2) == ("decode_hyb8r_kernel" if split else "decode_hyb8_kernel")
         assert_same(gpu_decode(net, pr, 2, 1, 20), want, 2, f"hyb8 split2={split}")
     net.set_option("hyb8_split", 1)
     for nr in (6, 7, 8):                          # rows of the rotated kernel's first push step
@@ -454,6 +456,11 @@ def test_kernel_selection(gb, c, l, rule, want):
     n_padded <= 4096 runs on a CTA pair (sos_tc2x2 / sos_tc3x2) unless
     GB_OPT_SOS_PAIR = 0."""
     net = gb.Net(c, l)
+    if rule == 0 and c <= 8 and c * 32 * ((l + 31) // 32) <= 1024 and (l + 31) // 32 in (1, 2, 4):
+        # an empty (sealed) W has density 0: sum-of-sum on the CUDA cores unless sos_bits = 0
+        net.seal()
+        assert net.decode_kernel(rule) == "sos_bits_kernel"
+        net.set_option("sos_bits", 0)
     if want in ("sos_tc2_kernel", "sos_tc3_kernel"):
         assert net.decode_kernel(rule) == want.replace("_kernel", "x2_kernel")
         net.set_option("sos_pair", 0)
@@ -599,6 +606,7 @@ def test_sos_pair_vs_single_cta(gb, c, l, m, e, gamma):
     msgs = gbgen.messages(500 + c + l, m, c, l)
     net = make_net(gb, msgs, c, l)
     pr, _ = gbgen.probes(501 + c, msgs, 1537, e, l, random_count=5)
+    net.set_option("sos_bits", 0)   # the tensor-core kernels
     res = {}
     for flag in ("1", "0"):
         net.set_option("sos_pair", int(flag))
@@ -721,6 +729,7 @@ def test_sos_cycle_exit_flag(gb, c, l, m, e, k, gamma, opts, kernel):
         pr, _ = gbgen.probes(801 + c, msgs, k, e, l, random_count=k // 3)
     w, _ = oracle.store(msgs, c, l)
     net = make_net(gb, msgs, c, l)
+    net.set_option("sos_bits", 0)   # reported name of the no-flag path; the flag never takes it
     for kk, v in opts.items():
         net.set_option(kk, v)
     assert net.decode_kernel(0) == kernel
@@ -771,6 +780,46 @@ def test_som_tensor_core_matches_oracle(gb, c, l, m, e, k):
     net.close()
 
 
+@pytest.mark.parametrize("c,l,m,e,gamma,k", [(8, 128, 5000, 4, 2, 3001), (8, 128, 5000, 4, 0, 700),
+                                             (8, 128, 2000, 5, 5, 513), (4, 16, 50, 2, 1, 1000),
+                                             (8, 64, 1500, 3, 1, 600), (7, 100, 3000, 3, 2, 777),
+                                             (3, 3, 4, 2, 1, 64), (8, 33, 300, 4, 3, 300),
+                                             (8, 128, 30000, 4, 2, 300)])
+def test_sos_bits_matches_oracle(gb, c, l, m, e, gamma, k):
+    """Sum-of-sum on the CUDA cores (sos_bits_kernel: the active neurons' rows added into
+    bit-sliced counters, winner-take-all plane by plane) against the oracle and the tensor-
+    core kernels, bit for bit: word counts 1 / 2 / 4, ragged L, gamma 0..5, T = 1 / 3 / 20,
+    invalid and random (non-stored) probes; random probes and dense W (M = 30000) push
+    probes past the 32-entry list / 6 counter planes, so the overflow list is exercised too
+    (decoded from the start by the CTA-pair tensor kernel in list mode, or by
+    decode_generic_kernel when the pair kernel is off)."""
+    msgs = gbgen.messages(1300 + c + l, m, c, l)
+    pr, _ = gbgen.probes(1301 + c, msgs, k, e, l, random_count=k // 4)
+    pr[1, 0] = l                       # invalid symbol
+    w, _ = oracle.store(msgs, c, l)
+    net = make_net(gb, msgs, c, l)
+    net.set_option("sos_bits", 1)
+    assert net.decode_kernel(0) == "sos_bits_kernel"
+    for T in (20, 3, 1):
+        want = oracle.decode(w, c, l, pr, 0, gamma=gamma, max_iters=T)
+        got = gpu_decode(net, pr, 0, gamma, T)
+        assert_same(got, want, 0, f"sos_bits c={c} l={l} m={m} T={T}")
+    net.set_option("sos_pair", 0)                  # overflow list -> generic kernel
+    assert_same(gpu_decode(net, pr, 0, gamma, T), want, 0, "sos_bits, overflow to the generic kernel")
+    net.set_option("sos_pair", 1)
+    net.set_option("sos_bits", 0)
+    other = gpu_decode(net, pr, 0, gamma, 1)
+    for x, y in zip(got, other):
+        np.testing.assert_array_equal(x, y)
+    # the period-2 exit keeps the tensor-core kernels (same results as the oracle's flag)
+    net.set_option("sos_bits", 1)
+    st, it, ss = net.decode(to_dev(pr), 0, gamma=gamma, max_iters=20, flags=gb.FLAG_CYCLE_EXIT)
+    torch.cuda.synchronize()
+    assert_same((st.cpu().numpy().view(np.uint32), it.cpu().numpy().view(np.uint16), ss.cpu().numpy()),
+                oracle.decode(w, c, l, pr, 0, gamma=gamma, max_iters=20, flags=oracle.CYCLE_EXIT), 0, "cycle exit")
+    net.close()
+
+
 @pytest.mark.parametrize("seed", range(24))
 def test_random_shapes_fuzz(gb, seed):
     """Seeded sweep over random shapes (C 2..16, L 1..300 incl. ragged and
@@ -796,7 +845,12 @@ def test_random_shapes_fuzz(gb, seed):
         w, _ = oracle.store(msgs, c, l) if m else (np.zeros((c * l, c * l), np.uint8), None)
         net = make_net(gb, msgs, c, l)
         tag = f"fuzz c={c} l={l} m={m} k={k} e={e} rule={rule} g={gamma} T={T} kernel={net.decode_kernel(rule)}"
-        assert_same(gpu_decode(net, pr, rule, gamma, T), oracle.decode(w, c, l, pr, rule, gamma, T), rule, tag)
+        want = oracle.decode(w, c, l, pr, rule, gamma, T)
+        assert_same(gpu_decode(net, pr, rule, gamma, T), want, rule, tag)
+        if rule == 0:   # sum-of-sum on the CUDA cores and on the tensor cores, both forced
+            for ob in (1, 0):
+                net.set_option("sos_bits", ob)
+                assert_same(gpu_decode(net, pr, rule, gamma, T), want, rule, tag + f" sos_bits={ob}")
         net.close()
 
 
