@@ -260,11 +260,14 @@ def symbols_agree(sym, state_dev, c, l, n=4096):
 
 def config_dict(args, cfg, ws):
     c, l, m, e, rule, k, desc = cfg
-    return {"workload": desc, "c": c, "l": l, "M": m, "erased": e, "rule": RULE_NAMES[rule],
-            "gamma": args.gamma, "max_iters": args.max_iters, "probes_per_gpu": k,
-            "global_batch": k * ws,
-            "parallelism": f"dp{ws} (probe shards; W stored on rank 0, packed rows broadcast over NCCL)",
-            "l2": l2_policy(c, l, k)[1], "seed": SEED}
+    d = {"workload": desc, "c": c, "l": l, "M": m, "erased": e, "rule": RULE_NAMES[rule],
+         "gamma": args.gamma, "max_iters": args.max_iters, "probes_per_gpu": k,
+         "global_batch": k * ws,
+         "parallelism": f"dp{ws} (probe shards; W stored on rank 0, packed rows broadcast over NCCL)",
+         "l2": l2_policy(c, l, k)[1], "seed": SEED}
+    if getattr(args, "opt", None):
+        d["kernel_options"] = list(args.opt)   # gb_set_option overrides (bit-exact kernel choices)
+    return d
 
 
 SM_COUNT, SM_CLOCK_GHZ = 148, 1.965   # B200 (B200_PROFILING.md); clocks sampled in the C3 line

@@ -32,7 +32,7 @@ KEYS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio",
         "smsp__average_warps_issue_stalled_mio_throttle_per_issue_active.ratio")
 # capture -> (summary name, traffic key)
-CAPS = {"prof_hyb": ("hyb", "c3"), "prof_sos": ("sos", "c2"), "prof_sosc4": ("sos_c4", "c4"),
+CAPS = {"prof_hyb": ("hyb", "c3"), "prof_sos": ("sos", "c2"), "prof_sosbits": ("sos_bits", "c2"), "prof_sosc4": ("sos_c4", "c4"),
         "prof_l2": ("l2", "c4"), "prof_store": ("store", "c5"), "prof_smem": ("smem", "c2som")}
 
 

@@ -18,7 +18,8 @@ tail -1 gpurun_out/bench_ref_$TAG.json | head -c 300; echo
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
 NCU="timeout 400 ncu --set full --clock-control none --import-source on"
 $NCU -k regex:decode_hyb8 -s 2 -c 1 -o gpurun_out/prof_hyb_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > /dev/null 2>&1
-$NCU -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 > /dev/null 2>&1
+$NCU -k regex:sos_tc -s 3 -c 1 -o gpurun_out/prof_sos_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 --opt sos_bits=0 > /dev/null 2>&1
+$NCU -k regex:sos_bits -s 3 -c 1 -o gpurun_out/prof_sosbits_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 0 --probes 1000000 > /dev/null 2>&1
 $NCU -k regex:sos_tc -s 1 -c 1 -o gpurun_out/prof_sosc4_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c4 --rule 0 --probes 100000 > /dev/null 2>&1
 $NCU -k regex:decode_l2t -s 1 -c 1 -o gpurun_out/prof_l2_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c4 --rule 2 --probes 1000000 > /dev/null 2>&1
 $NCU -k regex:decode_smem -s 3 -c 1 -o gpurun_out/prof_smem_$TAG python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --config c2 --rule 1 --probes 1000000 > /dev/null 2>&1
@@ -30,7 +31,7 @@ for M in 5000 10000 15000 20000 25000 30000; do
     timeout 400 python bench.py --steps 10 --config c2 --messages $M --rule $R --cpu-budget 6 --e2e-steps 2 >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
   done
 done
-for a in "--config c2 --rule 0 --probes 1000000" "--config c2 --rule 2 --probes 10000000" "--config c4 --rule 0" "--config c4 --rule 1" "--config c4 --rule 2" "--config s2 --rule 2" "--config s2 --rule 1" "--config s2 --rule 0"; do
+for a in "--config c2 --rule 0 --probes 1000000" "--config c2 --rule 0 --probes 1000000 --opt sos_bits=0" "--config c2 --rule 2 --probes 10000000" "--config c4 --rule 0" "--config c4 --rule 1" "--config c4 --rule 2" "--config s2 --rule 2" "--config s2 --rule 1" "--config s2 --rule 0"; do
   timeout 600 python bench.py --steps 10 --cpu-budget 6 --e2e-steps 2 $a >> gpurun_out/bench_rules_$TAG.jsonl 2>/dev/null
 done
 for R in 0 1 2; do
