@@ -64,13 +64,18 @@ __device__ __forceinline__ void score_wta2(const uint32_t (&va)[WC], const uint3
             pa[b][u] = ((gamma >> b) & 1u) ? va[u] : 0u;
             pb[b][u] = ((gamma >> b) & 1u) ? vb[u] : 0u;
         }
-    auto add = [&](uint32_t (&pl)[P][WC], const Blk &blk) {
-        const uint32_t *x = reinterpret_cast<const uint32_t *>(&blk);
+    // two rows per step: plane 0 takes both through a full adder (sum = p ^ x ^ y, carry =
+    // majority), the carry then ripples up -- 2P logic ops per word for two rows instead of 4P
+    auto add2 = [&](uint32_t (&pl)[P][WC], const Blk &bx, const Blk &by) {
+        const uint32_t *x = reinterpret_cast<const uint32_t *>(&bx);
+        const uint32_t *y = reinterpret_cast<const uint32_t *>(&by);
 #pragma unroll
         for (int u = 0; u < WC; ++u) {
-            uint32_t cy = x[u];
+            const uint32_t p0 = pl[0][u];
+            uint32_t cy = (p0 & x[u]) | (p0 & y[u]) | (x[u] & y[u]);
+            pl[0][u] = p0 ^ x[u] ^ y[u];
 #pragma unroll
-            for (int b = 0; b < P; ++b) {
+            for (int b = 1; b < P; ++b) {
                 const uint32_t t = pl[b][u] & cy;
                 pl[b][u] ^= cy;
                 cy = t;
@@ -79,13 +84,15 @@ __device__ __forceinline__ void score_wta2(const uint32_t (&va)[WC], const uint3
     };
     // the warp's largest count for every lane (no divergence); a lane past its own count adds the
     // zero row
-#pragma unroll 2
-    for (int e = 0; e < cntw; ++e) {
-        const uint32_t off = e < cnt ? lst[e * kNTb] : zoff;
-        const Blk xa = *reinterpret_cast<const Blk *>(w + off + ta);
-        const Blk xb = *reinterpret_cast<const Blk *>(w + off + tbb);
-        add(pa, xa);
-        add(pb, xb);
+    for (int e = 0; e < cntw; e += 2) {
+        const uint32_t o0 = e < cnt ? lst[e * kNTb] : zoff;
+        const uint32_t o1 = e + 1 < cnt ? lst[(e + 1) * kNTb] : zoff;
+        const Blk xa = *reinterpret_cast<const Blk *>(w + o0 + ta);
+        const Blk ya = *reinterpret_cast<const Blk *>(w + o1 + ta);
+        const Blk xb = *reinterpret_cast<const Blk *>(w + o0 + tbb);
+        const Blk yb = *reinterpret_cast<const Blk *>(w + o1 + tbb);
+        add2(pa, xa, ya);
+        add2(pb, xb, yb);
     }
     auto wta = [&](const uint32_t (&pl)[P][WC], uint32_t (&out)[WC]) {
         uint32_t cand[WC];
