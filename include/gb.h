@@ -109,7 +109,8 @@ enum {
                                   6..8 force it (bit-exact either way)               */
     GB_OPT_SOS_BITS = 8        /* -1 (default): sum-of-sum on the CUDA cores (active
                                   rows into bit-sliced counters) when W is sparse
-                                  (C <= 8, n_padded <= 1024, no cycle exit), else on
+                                  (density < 0.45, C <= 8, n_padded <= 1024, no
+                                  cycle exit), else on
                                   the tensor cores; 0 / 1 force it (bit-exact)       */
 };
 

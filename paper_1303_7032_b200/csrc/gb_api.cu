@@ -603,10 +603,10 @@ int64_t *Call::ovf(int64_t k) {
 }
 
 // W density below which sum-of-sum runs on the CUDA cores (gb_decode_sos_bits.cu).  Measured
-// crossover (c=8 l=128 e=4, 10^6 probes, sos_bits vs sos_tc2x2 ms): M=3k (d=0.17) 0.60 vs 1.92,
-// M=5k (0.26) 1.35 vs 2.51, M=6.5k (0.33) 1.76 vs 2.97, M=8k (0.39) 2.87 vs 3.45, M=10k (0.46)
-// 4.45 vs 3.81.
-constexpr double kSosBitsDensity = 0.4;
+// crossover (c=8 l=128 e=4, 10^6 probes, sos_bits vs sos_tc2x2 ms): M=3k (d=0.17) 0.52 vs 1.92,
+// M=5k (0.26) 0.95 vs 2.51, M=8k (0.39) 2.10 vs 3.45, M=10k (0.46) 3.65 vs 3.80, M=12k (0.52)
+// 5.08 vs 4.03.
+constexpr double kSosBitsDensity = 0.45;
 
 bool sos_bits_chosen(const gb_net *net, int gamma, int cyc) {
     const int ob = net->opt[kOptSosBits].load(std::memory_order_relaxed);
