@@ -1,9 +1,11 @@
 """Small decode/store workload for compute-sanitizer (memcheck / racecheck / synccheck).
 
 Covers every kernel family: store (scattered + privatised) + apply + seal, OR of packed
-partials, decode_hyb8 / decode_smem (both slot instances), decode_l2t + decode_l2 (list mode),
-SOS pair / streamed-A (incl. Lp = 512 with the state in the global scratch) / 4-warp / generic,
-the cycle-exit flag, and the tensor-core SOM kernel.
+partials, decode_hyb8 (sparse loop) / decode_hyb8r (rotated layout, every first-step row count) /
+decode_smem (both slot instances), decode_l2t + decode_l2 (list mode), SOS on the CUDA cores
+(sos_bits, with its overflow to the pair kernel in list mode and to the generic kernel) / pair /
+streamed-A (incl. Lp = 512 with the state in the global scratch) / 4-warp / generic, the
+cycle-exit flag, the tensor-core SOM kernel, and the host-buffer pipeline (3 streams).
 """
 import os
 import sys
@@ -38,7 +40,24 @@ for (c, l, m, k, e) in ((4, 16, 50, 300, 2), (8, 128, 5000, 700, 4), (12, 40, 50
         for split in (0, 1):
             net.set_option("hyb8_split", split)
             net.decode(probes, 2, gamma=1, max_iters=6)
+        for nr in (6, 7, 8):
+            net.set_option("hyb8_rows", nr)
+            net.decode(probes, 2, gamma=1, max_iters=6)
+        net.set_option("hyb8_rows", 0)
         net.set_option("hyb8_split", -1)
+        # sum-of-sum on the CUDA cores, forced, with random probes (overflow -> pair list mode,
+        # then -> generic with the pair off) and the tensor path forced
+        rp = torch.from_numpy(gbgen.probes(9, msgs, 400, 6, l, random_count=200)[0].view(np.int16)).cuda()
+        for ob, sp in ((1, 1), (1, 0), (0, 1)):
+            net.set_option("sos_bits", ob)
+            net.set_option("sos_pair", sp)
+            net.decode(rp, 0, gamma=1, max_iters=6)
+        net.set_option("sos_bits", -1)
+        net.set_option("sos_pair", 1)
+        # host buffers: the three-stream pipeline
+        ph = torch.from_numpy(pr.view(np.int16)).pin_memory()
+        out = net.alloc_outputs(k, device=False, pin=True)
+        net.decode(ph, 2, gamma=1, max_iters=6, out=out)
         part = gb.Net(c, l)
         part.store(torch.from_numpy(msgs[: m // 2].view(np.int16)).cuda())
         part.seal()
