@@ -217,6 +217,21 @@ int gb_bits(gb_net *net, uint32_t **wb, int64_t *nbytes);
 int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream);
 
 /*
+ * gb_or_bits_multimem -- the NVLS form of gb_or_bits:
+ * mc_bits is a MULTICAST address (a multicast object, e.g. torch symmetric
+ * memory's multicast_ptr, mapped over one n_padded x n_padded/32 uint32
+ * buffer per participating GPU, every rank's partial Wb at the same offset).
+ * One multimem.ld_reduce.or per word reads the OR over all GPUs' copies,
+ * reduced inside the NVSwitch, and sets those bits in W8 (w_ij |= ...).
+ * Every rank must have written its copy before the call (a barrier over the
+ * group); the caller keeps the buffers unchanged until the kernel is done.
+ * Unseals; stream-ordered.  GB_EINVAL for NULL or misaligned mc_bits; a
+ * non-multicast address fails at launch (GB_ECUDA).  Eq.(1) is an OR of
+ * cliques, so the result is the W of all shards.
+ */
+int gb_or_bits_multimem(gb_net *net, const uint32_t *mc_bits, void *stream);
+
+/*
  * gb_pack_upper -- the upper triangle of the sealed Wb, packed: for every
  * cluster pair a < b (lexicographic), the Lp x Wc words of Wb rows
  * a*Lp .. a*Lp+Lp-1, words b*Wc .. b*Wc+Wc-1, row-major.  W is symmetric

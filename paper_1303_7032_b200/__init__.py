@@ -31,6 +31,7 @@ LIB_PATH = os.environ.get("GB_LIB", os.path.join(_HERE, "libgb.so"))   # GB_LIB:
 
 # Every symbol include/gb.h declares (checked by tests/test_abi.py).
 EXPORTS = ("gb_create", "gb_destroy", "gb_clear", "gb_store", "gb_set_option", "gb_get_option", "gb_weights",
+           "gb_or_bits_multimem",
            "gb_weights_view", "gb_bits", "gb_or_bits", "gb_pack_upper", "gb_or_upper", "gb_seal", "gb_seal_status",
            "gb_decode", "gb_decode_ex", "gb_decode_symbols", "gb_info",
            "gb_launch_count", "gb_decode_kernel", "gb_last_error", "gb_version")
@@ -72,6 +73,7 @@ def lib() -> ctypes.CDLL:
         "gb_get_option": ([P, i32, ctypes.POINTER(i32)], i32),
         "gb_bits": ([P, PP, ctypes.POINTER(i64)], i32),
         "gb_or_bits": ([P, P, i64, P], i32),
+        "gb_or_bits_multimem": ([P, P, P], i32),
         "gb_pack_upper": ([P, P, ctypes.POINTER(i64), P], i32),
         "gb_or_upper": ([P, P, i64, P], i32),
         "gb_decode": ([P, P, i64, i32, i32, i32, P, P, P, P], i32),
@@ -215,6 +217,11 @@ class Net:
         assert bits.is_cuda and bits.is_contiguous() and tuple(bits.shape[-2:]) == (self.n_padded, self.nw)
         count = bits.numel() // (self.n_padded * self.nw)
         _check(lib().gb_or_bits(self._h, ctypes.c_void_p(bits.data_ptr()), count, _stream(stream)))
+
+    def or_bits_multimem(self, mc_ptr: int, stream=None):
+        """gb_or_bits_multimem: OR into W8 the packed matrices every GPU of a multicast group
+        holds at the multicast address mc_ptr (NVLS reduction, one multimem.ld_reduce.or per word)."""
+        _check(lib().gb_or_bits_multimem(self._h, ctypes.c_void_p(mc_ptr), _stream(stream)))
 
     def upper_words(self) -> int:
         n = ctypes.c_int64()

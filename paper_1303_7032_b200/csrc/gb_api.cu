@@ -334,6 +334,17 @@ int gb_or_bits(gb_net *net, const uint32_t *bits, int64_t count, void *stream) {
     return GB_OK;
 }
 
+int gb_or_bits_multimem(gb_net *net, const uint32_t *mc_bits, void *stream) {
+    if (!net) return fail(GB_EINVAL, "gb_or_bits_multimem: net is NULL");
+    if (!mc_bits) return fail(GB_EINVAL, "gb_or_bits_multimem: mc_bits is NULL");
+    if ((uintptr_t)mc_bits & 3u) return fail(GB_EINVAL, "gb_or_bits_multimem: mc_bits not 4-byte aligned");
+    DeviceGuard g(net->device);
+    net->sealed = false;
+    gb::Call cl(net, (cudaStream_t)stream);
+    GB_CUDA(gb::launch_or_multimem(cl, mc_bits), "gb_or_bits_multimem: launch");
+    return GB_OK;
+}
+
 int gb_pack_upper(gb_net *net, uint32_t *out, int64_t *nwords, void *stream) {
     if (!net) return fail(GB_EINVAL, "gb_pack_upper: net is NULL");
     if (nwords) *nwords = gb::upper_words(net->s);

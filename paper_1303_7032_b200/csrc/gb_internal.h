@@ -169,6 +169,7 @@ int option_default(int o);
 cudaError_t launch_store(Call &cl, const uint16_t *msgs, int64_t m);
 cudaError_t launch_seal(gb_net *net, cudaStream_t st);
 cudaError_t launch_or_bits(Call &cl, const uint32_t *bits, int64_t count);
+cudaError_t launch_or_multimem(Call &cl, const uint32_t *mc);
 int64_t upper_words(const Shape &s);   // words of one packed upper-triangle set
 cudaError_t launch_pack_upper(Call &cl, uint32_t *out);
 cudaError_t launch_or_upper(Call &cl, const uint32_t *sets, int64_t count);

@@ -394,6 +394,40 @@ cudaError_t launch_or_bits(Call &cl, const uint32_t *bits, int64_t count) {
     return cudaGetLastError();
 }
 
+// NVLS merge: every rank holds its partial packed rows Wb at the same offset of
+// a buffer bound to a multicast object; one multimem.ld_reduce.or per word returns the OR over
+// all ranks' copies (reduced in the NVSwitch), and the bits are set in W8 as apply_kernel does.
+__global__ void or_multimem_kernel(Shape s, const uint32_t *mc, uint8_t *__restrict__ w8) {
+    const int64_t total = (int64_t)s.np * s.nw;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t bits;
+        asm volatile("multimem.ld_reduce.relaxed.sys.global.or.b32 %0, [%1];" : "=r"(bits) : "l"(mc + idx) : "memory");
+        if (!bits) continue;
+        const int64_t i = idx / s.nw, w = idx - i * s.nw;
+        uint4 *p = reinterpret_cast<uint4 *>(w8 + i * s.np + w * 32);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 v = p[h];
+            uint32_t q[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t nib = (bits >> (16 * h + 4 * k)) & 15u;
+                q[k] |= (nib & 1u) | ((nib & 2u) << 7) | ((nib & 4u) << 14) | ((nib & 8u) << 21);
+            }
+            p[h] = make_uint4(q[0], q[1], q[2], q[3]);
+        }
+    }
+}
+
+cudaError_t launch_or_multimem(Call &cl, const uint32_t *mc) {
+    const int64_t total = (int64_t)cl.net->s.np * cl.net->s.nw;
+    const int64_t grid = std::min<int64_t>((total + 255) / 256, (int64_t)cl.net->sm_count * 8);
+    or_multimem_kernel<<<(unsigned)grid, 256, 0, cl.st>>>(cl.net->s, mc, cl.net->w8);
+    cl.launched();
+    return cudaGetLastError();
+}
+
 int64_t upper_words(const Shape &s) { return (int64_t)s.Lp * s.Wc * s.C * (s.C - 1) / 2; }
 
 cudaError_t launch_pack_upper(Call &cl, uint32_t *out) {

@@ -217,3 +217,106 @@ def sharded_store_bits(net, msgs_shard, group=None, stream=None):
         allb = gather_bits(net.bits(), group)
         net.or_bits(allb, stream)
     net.seal(stream, check=False)
+
+
+_MC = {}   # (group name, words, device) -> (buffer, handle): one allocation per shape
+
+
+class _LocalMulticast:
+    """A one-GPU multicast object (CUDA driver multicast API through cuda-python): the
+    group-of-one case, where no handle has to be exported to other processes.  Gives the
+    same (buffer, handle) pair as torch symmetric memory: ``multicast_ptr`` and ``barrier``."""
+
+    def __init__(self, words: int, device):
+        from cuda.bindings import driver as cu
+        dev = torch.device(device).index or 0
+        torch.cuda.init()
+
+        def ok(r):
+            err = r[0] if isinstance(r, tuple) else r
+            if err != cu.CUresult.CUDA_SUCCESS:
+                raise RuntimeError(f"CUDA driver: {err}")
+            return r[1] if isinstance(r, tuple) and len(r) == 2 else r
+        size = words * 4
+        prop = cu.CUmulticastObjectProp()
+        prop.numDevices = 1
+        prop.handleTypes = 0
+        prop.size = size
+        gran = ok(cu.cuMulticastGetGranularity(prop, cu.CUmulticastGranularity_flags.CU_MULTICAST_GRANULARITY_RECOMMENDED))
+        size = (size + gran - 1) // gran * gran
+        prop.size = size
+        self.mc = ok(cu.cuMulticastCreate(prop))
+        ok(cu.cuMulticastAddDevice(self.mc, ok(cu.cuDeviceGet(dev))))
+        ap = cu.CUmemAllocationProp()
+        ap.type = cu.CUmemAllocationType.CU_MEM_ALLOCATION_TYPE_PINNED
+        ap.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        ap.location.id = dev
+        self.mem = ok(cu.cuMemCreate(size, ap, 0))
+        ok(cu.cuMulticastBindMem(self.mc, 0, self.mem, 0, size, 0))
+        acc = cu.CUmemAccessDesc()
+        acc.location.type = cu.CUmemLocationType.CU_MEM_LOCATION_TYPE_DEVICE
+        acc.location.id = dev
+        acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
+        self.uva = ok(cu.cuMemAddressReserve(size, gran, 0, 0))
+        ok(cu.cuMemMap(self.uva, size, 0, self.mem, 0))
+        ok(cu.cuMemSetAccess(self.uva, size, [acc], 1))
+        self.mva = ok(cu.cuMemAddressReserve(size, gran, 0, 0))
+        ok(cu.cuMemMap(self.mva, size, 0, self.mc, 0))
+        ok(cu.cuMemSetAccess(self.mva, size, [acc], 1))
+        self.multicast_ptr = int(self.mva)
+
+        class _Arr:
+            pass
+        a = _Arr()
+        a.__cuda_array_interface__ = {"shape": (words,), "typestr": "<i4", "data": (int(self.uva), False),
+                                      "version": 3, "strides": None}
+        self.buffer = torch.as_tensor(a, device=torch.device("cuda", dev))
+
+    def barrier(self, channel=0):
+        torch.cuda.synchronize()
+
+
+def multicast_buffer(words: int, device, group=None):
+    """A buffer of ``words`` int32 per GPU of the group with its multicast (NVLS) mapping:
+    torch symmetric memory (its rendezvous exports the multicast handle to the other ranks),
+    else for a group of one a local multicast object; None when neither is available."""
+    import torch.distributed._symmetric_memory as symm_mem
+    g = group if group is not None else dist.group.WORLD
+    key = (g.group_name, words, str(device))
+    if key not in _MC:
+        buf = symm_mem.empty(words, dtype=torch.int32, device=device)
+        hdl = symm_mem.rendezvous(buf, g.group_name)
+        if getattr(hdl, "multicast_ptr", 0):
+            _MC[key] = (buf, hdl)
+        elif dist.get_world_size(g) == 1:
+            try:
+                loc = _LocalMulticast(words, device)
+                _MC[key] = (loc.buffer, loc)
+            except Exception:   # no multicast on this GPU / driver
+                _MC[key] = None
+        else:
+            _MC[key] = None
+    return _MC[key]
+
+
+def sharded_store_nvls(net, msgs_shard, group=None, stream=None):
+    """The NVLS form of sharded_store_bits: each rank stores its shard, seals
+    (packing the partial Wb) and copies Wb into its symmetric buffer; after a barrier, one
+    kernel per rank (gb_or_bits_multimem) reads the OR of all ranks' partials through the
+    multicast address -- reduced inside the NVSwitch -- into its cleared W8; seal.  No data
+    moves through NCCL.  Returns False (nothing done) when the group has no multicast support."""
+    mc = multicast_buffer(net.n_padded * net.nw, torch.device("cuda", net.device), group)
+    if mc is None:
+        return False
+    buf, hdl = mc
+    net.clear(stream)
+    if msgs_shard.shape[0]:
+        net.store(msgs_shard, stream)
+    net.seal(stream, check=False)
+    buf.view(net.n_padded, net.nw).copy_(net.bits())
+    hdl.barrier(channel=0)                 # every rank's partial is in place
+    net.clear(stream)
+    net.or_bits_multimem(hdl.multicast_ptr, stream)
+    hdl.barrier(channel=0)                 # every rank has read the partials (buffer reusable)
+    net.seal(stream, check=False)
+    return True
