@@ -525,6 +525,20 @@ def main():
                                        "note": "dense-contraction ops the tensor-core path executes for the "
                                                "same rounds; this kernel adds only the active rows"}
         wpp = ncu_entry(kernel, args.config).get("smem_wavefronts_per_probe")
+        ipp = ncu_entry(kernel, args.config).get("warp_instructions_per_probe")
+        if kernel == "sos_bits_kernel" and ipp:
+            # its binding on-chip resource: issue slots (4 warp-instructions per SM per clock);
+            # instructions per probe from the committed ncu capture, time from this run
+            sm_clk = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("sm_max_mhz", 1965.0)) \
+                if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 1965.0
+            per_s = ipp * k / (dec_ms / 1e3)
+            peak_is = 4 * torch.cuda.get_device_properties(dev).multi_processor_count * sm_clk * 1e6
+            roof["onchip"] = {"resource": "issue slots (4 warp-instructions per SM per clock)",
+                              "warp_instructions_per_probe": ipp, "achieved_per_s": per_s, "peak_per_s": peak_is,
+                              "frac": per_s / peak_is, "source": ncu_entry(kernel, args.config).get("source"),
+                              "note": "instructions per probe from the committed ncu capture named in source "
+                                      "(ncu cannot run inside the timed bench); time from this run"}
+            wpp = None
         if wpp:
             # the binding on-chip resource of the bit kernels: shared-memory wavefronts through the
             # LSU data pipe (one wavefront per SM per clock); per-probe count from the ncu capture

@@ -48,7 +48,8 @@ def to_bytes(u, v):
 
 
 # probes per launch of the captures whose shared-memory wavefronts are reported per probe
-PROBES = {"prof_hyb": 10_000_000, "prof_smem": 1_000_000}   # kernels whose W rows live in shared memory
+PROBES = {"prof_hyb": 10_000_000, "prof_smem": 1_000_000,     # kernels whose W rows live in shared memory
+          "prof_sosbits": 1_000_000}
 traffic = {}
 for cap, (name, cfg) in CAPS.items():
     rep = os.path.join(G, f"{cap}_{TAG}.ncu-rep")
@@ -70,6 +71,8 @@ for cap, (name, cfg) in CAPS.items():
             wf = float(d["l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"][1].replace(",", ""))
             traffic[tkey]["smem_wavefronts_per_probe"] = wf / PROBES[cap]
             traffic[tkey]["probes_in_capture"] = PROBES[cap]
+        if cap in PROBES and "smsp__inst_executed.sum" in d:
+            traffic[tkey]["warp_instructions_per_probe"] = float(d["smsp__inst_executed.sum"][1].replace(",", "")) / PROBES[cap]
 if traffic:
     json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
 for src, dst in ((f"bench_full_{TAG}.json", f"{RND}_bench_c3.json"),

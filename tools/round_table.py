@@ -22,7 +22,8 @@ def row(d):
     if r:
         roof = "%.3f of %.1f %s" % (r["frac"], r["peak"], r["unit"])
         if r.get("onchip"):
-            roof += "; on-chip %.2f of the LSU wavefront peak" % r["onchip"]["frac"]
+            res = "issue-slot" if "issue" in r["onchip"].get("resource", "") else "LSU wavefront"
+            roof += "; on-chip %.2f of the %s peak" % (r["onchip"]["frac"], res)
         if r.get("int8_equivalent"):
             ie = r["int8_equivalent"]
             roof += "; int8-equivalent %.0f TOPS (%.2f of the int8 peak)" % (ie["tops"], ie["tops"] / ie["int8_peak_tops"])
