@@ -230,7 +230,8 @@ sos_bits_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__rest
         bool go = active;
         if (active && (cnt > kList || smax >= 64u)) {
             // a large active set (e.g. a cluster whose max was 0 turned whole, R4): the probe is
-            // decoded from the start by the generic kernel (list mode), exact either way
+            // queued and decoded from the start by the CTA-pair kernel in list mode (the generic
+            // kernel when the pair is off), exact either way
             ovf[atomicAdd(ovf_count, 1ull)] = p;
             refill();
             go = false;

@@ -784,13 +784,14 @@ def test_som_tensor_core_matches_oracle(gb, c, l, m, e, k):
                                              (8, 128, 2000, 5, 5, 513), (4, 16, 50, 2, 1, 1000),
                                              (8, 64, 1500, 3, 1, 600), (7, 100, 3000, 3, 2, 777),
                                              (3, 3, 4, 2, 1, 64), (8, 33, 300, 4, 3, 300),
-                                             (8, 128, 30000, 4, 2, 300)])
+                                             (8, 128, 30000, 4, 2, 300), (8, 128, 5000, 4, 40, 300)])
 def test_sos_bits_matches_oracle(gb, c, l, m, e, gamma, k):
     """Sum-of-sum on the CUDA cores (sos_bits_kernel: the active neurons' rows added into
     bit-sliced counters, winner-take-all plane by plane) against the oracle and the tensor-
     core kernels, bit for bit: word counts 1 / 2 / 4, ragged L, gamma 0..5, T = 1 / 3 / 20,
     invalid and random (non-stored) probes; random probes and dense W (M = 30000) push
-    probes past the 32-entry list / 6 counter planes, so the overflow list is exercised too
+    probes past the 32-entry list / 6 counter planes (and gamma = 40 every probe: a score
+    could reach 64), so the overflow list is exercised too
     (decoded from the start by the CTA-pair tensor kernel in list mode, or by
     decode_generic_kernel when the pair kernel is off)."""
     msgs = gbgen.messages(1300 + c + l, m, c, l)
