@@ -790,8 +790,9 @@ def test_sos_bits_matches_oracle(gb, c, l, m, e, gamma, k):
     bit-sliced counters, winner-take-all plane by plane) against the oracle and the tensor-
     core kernels, bit for bit: word counts 1 / 2 / 4, ragged L, gamma 0..5, T = 1 / 3 / 20,
     invalid and random (non-stored) probes; random probes and dense W (M = 30000) push
-    probes past the 32-entry list / 6 counter planes (and gamma = 40 every probe: a score
-    could reach 64), so the overflow list is exercised too
+    probes past the 32-entry list / 6 counter planes (gamma = 40 puts every probe on the
+    6-plane counters and those with 24+ active neurons past them), so the overflow list is
+    exercised too
     (decoded from the start by the CTA-pair tensor kernel in list mode, or by
     decode_generic_kernel when the pair kernel is off)."""
     msgs = gbgen.messages(1300 + c + l, m, c, l)
