@@ -409,6 +409,7 @@ def test_metric_config_full_size_sampled(gb):
     msgs = gbgen.messages(0x5EED, m, c, l)
     pr, src = gbgen.probes(0x5EED + 1, msgs, k, 4, l)
     net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(2) == "decode_hyb8r_kernel"   # W dense: the rotated-layout kernel
     prd = to_dev(pr)
     st, it, ss = net.decode(prd, 2, gamma=2, max_iters=20)
     torch.cuda.synchronize()
@@ -490,6 +491,31 @@ def test_config2_full_size_sampled(gb, rule):
         w, _ = oracle.store(msgs, c, l)
         assert_same((st[idx], it[idx], ss[idx]), oracle.decode(w, c, l, pr[idx], rule, 2, 20), rule,
                     f"config2 M={m} sampled")
+
+
+def test_config2_sos_full_batch_both_paths(gb):
+    """The bench's C2 sum-of-sum line at its size (c=8 l=128 M=5k e=4, K=10^6, gamma 2): the
+    CUDA-core kernel for sparse states (the default at this density) and the tensor-core
+    pair kernel give identical states, rounds and status for every probe of the batch, and
+    300 sampled probes equal the oracle."""
+    c, l, m, k = 8, 128, 5000, 1_000_000
+    msgs = gbgen.messages(0x5EED + m, m, c, l)
+    pr, _ = gbgen.probes(0x5EED + m + 1, msgs, k, 4, l)
+    net = make_net(gb, msgs, c, l)
+    assert net.decode_kernel(0) == "sos_bits_kernel"
+    prd = to_dev(pr)
+    a = net.decode(prd, 0, gamma=2, max_iters=20)
+    net.set_option("sos_bits", 0)
+    assert net.decode_kernel(0) == "sos_tc2x2_kernel"
+    b = net.decode(prd, 0, gamma=2, max_iters=20)
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+    idx = np.sort(np.random.default_rng(5).choice(k, 300, replace=False))
+    w, _ = oracle.store(msgs, c, l)
+    got = (a[0][idx].cpu().numpy().view(np.uint32), a[1][idx].cpu().numpy().view(np.uint16), a[2][idx].cpu().numpy())
+    assert_same(got, oracle.decode(w, c, l, pr[idx], 0, 2, 20), 0, "config2 SOS sampled")
+    net.close()
 
 
 def test_config4_full_size_sampled(gb):
