@@ -211,8 +211,14 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
         if (RULE == GB_HYBRID && nslot == 0) {
             status = GB_CONVERGED;
         } else {
+            // from round 2 on only the pairs whose source slot changed in the previous round: a
+            // pair whose source kept its candidates removes nothing (after the round that last
+            // evaluated it, the target's candidates lie inside the OR of the rows it read, and
+            // those rows are still candidates)
+            uint32_t chg = 0xFFFFFFFFu;
             while (it < T) {
                 bool changed = false;
+                uint32_t chgn = 0u;
                 uint32_t fulln = fullm;   // the round's pushes read the old state: update after it
                 for (int t = 0; t < nslot; ++t) {
                     const int ct = slot_c(t);
@@ -224,7 +230,7 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                         any |= alive[u];
                     }
                     for (int si = 0; si < nslot && any; ++si) {
-                        if (si == t) continue;
+                        if (si == t || !((chg >> si) & 1u)) continue;
                         const uint32_t *base = wb + (size_t)(slot_c(si) * LP) * nw + ct * WC;
                         uint32_t rem[WC];
                         uint32_t left = 0u;
@@ -278,12 +284,14 @@ decode_l2t_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__re
                     }
 #pragma unroll
                     for (int u = 0; u < WC; ++u) {
+                        if (alive[u] != X[(t * WC + u) * NT + tid]) chgn |= 1u << t;
                         changed |= (alive[u] != X[(t * WC + u) * NT + tid]);
                         Xn[(t * WC + u) * NT + tid] = alive[u];
                         if (alive[u] != rmask[u]) fulln &= ~(1u << t);
                     }
                 }
                 fullm = fulln;
+                chg = chgn;
                 if (changed)
                     for (int w = 0; w < nslot * WC; ++w) X[w * NT + tid] = Xn[w * NT + tid];
                 ++it;

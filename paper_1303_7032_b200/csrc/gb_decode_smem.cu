@@ -220,7 +220,11 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
         if (RULE == GB_HYBRID && nslot == 0) {
             status = GB_CONVERGED;
         } else {
-            // ---- a6 rounds
+            // ---- a6 rounds.  From round 2 on only the pairs whose source slot changed in the
+            // previous round are evaluated: a pair whose source kept its candidates removes
+            // nothing (after the round that last evaluated it, the target's candidates lie inside
+            // the OR of the rows it read, and those rows are still candidates).
+            uint32_t chg = 0xFFu;
             if constexpr (MAXS == 4) {
                 while (it < T) {
                     uint32_t xn[4][WC];
@@ -237,7 +241,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             }
 #pragma unroll
                             for (int sidx = 0; sidx < 4; ++sidx) {
-                                if (sidx < (int)nslot && sidx != t && any) {
+                                if (sidx < (int)nslot && sidx != t && any && ((chg >> sidx) & 1u)) {
                                     const uint32_t c2 = (slots >> (4 * sidx)) & 15u;
                                     uint32_t h[WC];
 #pragma unroll
@@ -284,11 +288,13 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                         }
                     }
                     bool changed = false;
+                    chg = 0u;
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         if (t < (int)nslot) {
 #pragma unroll
                             for (int u = 0; u < WC; ++u) {
+                                if (xr[t][u] != xn[t][u]) chg |= 1u << t;
                                 changed |= (xr[t][u] != xn[t][u]);
                                 xr[t][u] = xn[t][u];
                                 if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
@@ -314,7 +320,7 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                             any |= alive[u];
                         }
                         for (unsigned sidx = 0; sidx < nslot && any; ++sidx) {
-                            if ((int)sidx == t) continue;
+                            if ((int)sidx == t || !((chg >> sidx) & 1u)) continue;
                             const int c2 = (slots >> (4 * sidx)) & 15;
                             uint32_t h[WC];
 #pragma unroll
@@ -369,12 +375,14 @@ decode_smem_kernel(Shape s, const uint32_t *__restrict__ wb, const uint16_t *__r
                         for (int u = 0; u < WC; ++u) xn[t][u] = alive[u];
                     }
                 }
+                chg = 0u;
 #pragma unroll
                 for (int t = 0; t < MAXS; ++t) {
                     if (t < (int)nslot) {
 #pragma unroll
                         for (int u = 0; u < WC; ++u) {
                             uint32_t *a = &X[(t * WC + u) * NT + tid];
+                            if (*a != xn[t][u]) chg |= 1u << t;
                             changed |= (*a != xn[t][u]);
                             *a = xn[t][u];
                             if (!xn[t][u]) nzall &= ~(1u << (t * WC + u));
