@@ -107,11 +107,11 @@ enum {
     GB_OPT_HYB8_ROWS = 7,      /* 0 (default): rows of the rotated-layout hybrid
                                   kernel's first push step chosen by W's density;
                                   6..8 force it (bit-exact either way)               */
-    GB_OPT_SOS_BITS = 8        /* -1 (default): sum-of-sum on the CUDA cores (active
-                                  rows into bit-sliced counters) when W is sparse
-                                  (density < 0.45, C <= 8, n_padded <= 1024, no
-                                  cycle exit), else on
-                                  the tensor cores; 0 / 1 force it (bit-exact)       */
+    GB_OPT_SOS_BITS = 8        /* -1 (default): sum-of-sum on the CUDA cores (the
+                                  active rows into bit-sliced counters) when W is
+                                  sparse (density < 0.45; C <= 8, n_padded <= 1024,
+                                  no cycle exit), else on the tensor cores; 0 / 1
+                                  force it (bit-exact either way)                    */
 };
 
 /* gb_decode_ex flags. */
